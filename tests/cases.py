@@ -1,0 +1,74 @@
+"""Shared run configurations for the parity tests.
+
+The same cases (sources, seeds, parameters) are what tests/golden/make_golden.py
+ran through the reference.  Sources come from this package's host sampling
+module; the stream SHA-256 stored in each fixture proves they reproduce the
+reference's signal stream exactly.
+"""
+
+from __future__ import annotations
+
+import functools
+import os
+
+import numpy as np
+
+from paper_1503_08294_b200.sampling import CloudSource, SphereSource, TorusSource
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@functools.lru_cache(maxsize=None)
+def clouds():
+    rng0 = np.random.Generator(np.random.Philox(2026))
+    sph = SphereSource(1.0).sample(rng0, 10_000)
+    tor = TorusSource(2.0, 0.5).sample(rng0, 100_000)
+    return sph, tor
+
+
+@functools.lru_cache(maxsize=None)
+def hemisphere_cloud():
+    rng = np.random.Generator(np.random.Philox(99))
+    pts = SphereSource(1.0).sample(rng, 20_000)
+    return pts[pts[:, 2] >= 0.0]
+
+
+CASES = {
+    "sphere_exec": dict(source=("sphere", 1.0), seed=3,
+                        params=dict(theta0=0.35, max_signals=120_000)),
+    "cfg1": dict(source=("cloud", "sphere10k"), seed=7,
+                 params=dict(theta0=0.2, batch_floor=64, batch_cap=64, max_signals=5_000_000)),
+    "cfg2": dict(source=("cloud", "torus100k"), seed=7,
+                 params=dict(theta0=0.2, batch_floor=1024, batch_cap=1024, max_signals=12_000_000)),
+    "stress": dict(source=("torus", 2.0, 0.5), seed=11,
+                   params=dict(theta0=0.25, max_age=12, ring_patience=3, rho=0.7,
+                               stale_factor=1, batch_floor=64, batch_cap=512,
+                               max_signals=80_000)),
+    "boundary": dict(source=("cloud", "hemisphere"), seed=5,
+                     params=dict(theta0=0.3, allow_boundary=True, max_signals=150_000)),
+    "paper_rule": dict(source=("cloud", "torus100k"), seed=21,
+                       params=dict(theta0=0.15, max_signals=200_000)),
+}
+
+
+def make_source(spec):
+    kind = spec[0]
+    if kind == "sphere":
+        return SphereSource(spec[1])
+    if kind == "torus":
+        return TorusSource(spec[1], spec[2])
+    if kind == "cloud":
+        sph, tor = clouds()
+        pts = {"sphere10k": sph, "torus100k": tor, "hemisphere": hemisphere_cloud()}[spec[1]]
+        return CloudSource(pts, label=spec[1])
+    raise ValueError(spec)
+
+
+def load_golden(name):
+    path = os.path.join(GOLDEN, f"run_{name}.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def same_numpy(blob) -> bool:
+    return str(blob["numpy_version"]) == np.__version__
