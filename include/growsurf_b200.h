@@ -1,0 +1,200 @@
+/*
+ * growsurf_b200.h -- C ABI of the B200-native multi-signal growing network.
+ *
+ * Plain C types only (no torch, no CUDA runtime types): pointers, sizes and
+ * an opaque `void *stream` (a cudaStream_t, NULL = the context's own stream).
+ * Every entry point returns a gs_status; gs_last_error() returns a
+ * thread-local message for the last failure on the calling thread.
+ *
+ * Reference interfaces each group replaces (paths under the reference's
+ * pkg/src/growsurf/):
+ *
+ *   Kernel-backend protocol (kernels/__init__.py:6-7, 26-44)
+ *     gs_best_two_single      <- _scan.pyx:14-36   best_two_single
+ *     gs_scan_best_two_into   <- _scan.pyx:39-98   scan_best_two_into
+ *   Batched find on device data (multi.py:58-69 _scan_batch,
+ *   parallel.py:63-88 _parallel_scan): gs_find_device
+ *   Device-resident multi-signal engine (multi.py:99-202 resolve_and_update /
+ *   run_multi, engine.py:283-365 update_single / is_converged, network.py
+ *   Network accessors): gs_engine_*
+ *
+ * Threading: a gs_ctx owns one CUDA stream and scratch buffers and
+ * serialises its own calls with an internal mutex, so the reference's
+ * "disjoint output slices may be filled from parallel threads" contract
+ * (_scan.pyx:49-50, parallel.py:78-87) holds.  A gs_engine is
+ * single-threaded, like the reference Network (network.py:74).
+ */
+#ifndef GROWSURF_B200_H
+#define GROWSURF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GS_OK = 0,
+  GS_VALUE_ERROR = 1, /* ValueError in the reference (_scan.pyx:56-61, engine.py:71-91) */
+  GS_STATE_ERROR = 2, /* StateError (network.py:30, multi.py:60-61, engine.py:299-300) */
+  GS_CUDA_ERROR = 3,  /* no device, launch or copy failure */
+  GS_UNKNOWN_UNIT = 4 /* UnknownUnitError (network.py:26, 438-442) */
+} gs_status;
+
+const char *gs_last_error(void);
+const char *gs_version(void);
+
+/* ------------------------------------------------------------------ */
+/* context                                                              */
+
+typedef struct gs_ctx gs_ctx;
+
+gs_status gs_ctx_create(int device, gs_ctx **out);
+void gs_ctx_destroy(gs_ctx *ctx);
+/* Number of SMs of the context's device (grid sizing, roofline). */
+int gs_ctx_sm_count(const gs_ctx *ctx);
+
+/* ------------------------------------------------------------------ */
+/* kernel-backend protocol: host buffers, synchronous                   */
+
+/* best_two_single(pos, n, x, y, z) -> (r1, r2, d2_1, d2_2); rows are -1 and
+ * distances +inf where fewer than two units exist (fallback.py:21-30).
+ * pos: n_rows x 3 float64, C-contiguous; requires n <= n_rows. */
+gs_status gs_best_two_single(gs_ctx *ctx, const double *pos, int64_t n_rows, int64_t n, double x,
+                             double y, double z, int64_t *r1, int64_t *r2, double *d2_1,
+                             double *d2_2);
+
+/* scan_best_two_into(pos, n, signals, out_idx, out_d2, tile): for each of the
+ * m signals, the ROWS of the nearest and second-nearest of the first n rows
+ * of pos and their squared distances, lexicographic on (d^2, row) with
+ * d^2 = ((dx*dx + dy*dy) + dz*dz) in IEEE binary64 (no contraction).
+ * out_idx: out_rows x 2 int64, out_d2: out_d2_rows x 2 float64, written for
+ * [0, m).  GS_VALUE_ERROR when n > n_rows, an output is shorter than m, or
+ * tile < 1; tile never changes the result. */
+gs_status gs_scan_best_two_into(gs_ctx *ctx, const double *pos, int64_t n_rows, int64_t n,
+                                const double *signals, int64_t m, int64_t *out_idx,
+                                int64_t out_rows, double *out_d2, int64_t out_d2_rows,
+                                int64_t tile);
+
+/* ------------------------------------------------------------------ */
+/* batched find on device buffers (asynchronous on `stream`)            */
+
+typedef enum {
+  GS_FIND_EXACT = 0,  /* FP64 scan, the reference arithmetic */
+  GS_FIND_FILTER = 1, /* FP32 top-3 filter + certified FP64 re-check (bit-identical output) */
+  GS_FIND_AUTO = 2
+} gs_find_mode;
+
+/* d_pos: n x 3 float64 (device), d_sig: m x 3 float64 (device);
+ * d_idx: m x 2 int64 rows, d_d2: m x 2 float64 (device).  Returns without
+ * synchronising.  *fallbacks (optional, host) receives, after the next
+ * synchronisation of `stream`, the number of signals the filter could not
+ * certify and re-scanned exactly. */
+gs_status gs_find_device(gs_ctx *ctx, const double *d_pos, int64_t n, const double *d_sig,
+                         int64_t m, int64_t *d_idx, double *d_d2, int mode, void *stream);
+/* Signals re-scanned exactly by the last GS_FIND_FILTER call on this ctx (syncs). */
+gs_status gs_find_last_fallbacks(gs_ctx *ctx, int64_t *count);
+
+/* ------------------------------------------------------------------ */
+/* device-resident multi-signal engine                                  */
+
+typedef struct {
+  double eps_b, eps_n, theta0;
+  int64_t max_age;
+  double tau_b, tau_n, h_t, rho;
+  int64_t ring_patience;
+  int32_t allow_boundary;
+  int32_t find_mode; /* gs_find_mode */
+  int64_t stale_factor;
+} gs_params;
+
+typedef struct {
+  int64_t processed, discarded, inserted; /* BatchOutcome (multi.py:35-41) */
+  int64_t units, edges, next_id;          /* Network.unit_count / edge_count / next_id */
+  int64_t converged;                      /* is_converged after the batch (engine.py:358-365) */
+  int64_t tick;                           /* RunState.tick */
+  int64_t events;                         /* signals executed on the serial event path */
+  int64_t windows;                        /* parallel windows used by the batch */
+  int64_t error;                          /* device error code (0 = none) */
+  int64_t max_degree;                     /* largest unit degree seen (capacity check) */
+} gs_batch_stats;
+
+typedef struct gs_engine gs_engine;
+
+gs_status gs_engine_create(gs_ctx *ctx, const gs_params *params, int64_t capacity_hint,
+                           gs_engine **out);
+void gs_engine_destroy(gs_engine *eng);
+
+/* Network.add_unit (network.py:208-230): hab 1, no edges; returns the id. */
+gs_status gs_engine_add_unit(gs_engine *eng, double x, double y, double z, double threshold,
+                             int64_t *id);
+/* Network.connect_or_reset (network.py:261-282); *created = 1 if new. */
+gs_status gs_engine_connect_or_reset(gs_engine *eng, int64_t a, int64_t b, int32_t *created);
+/* Network.remove_unit (network.py:232-240). */
+gs_status gs_engine_remove_unit(gs_engine *eng, int64_t id);
+/* Network.remove_edge (network.py:284-292). */
+gs_status gs_engine_remove_edge(gs_engine *eng, int64_t a, int64_t b);
+/* Network.age_incident_edges(b, increment, exclude or -1) (network.py:294-319). */
+gs_status gs_engine_age_incident_edges(gs_engine *eng, int64_t b, int64_t increment,
+                                       int64_t exclude, int64_t *top);
+/* Network.prune(max_age) (network.py:321-369). */
+gs_status gs_engine_prune(gs_engine *eng, int64_t max_age, int64_t *pruned_edges,
+                          int64_t *units_removed);
+/* Overwrite one unit's habituation / position (tests set net._hab directly). */
+gs_status gs_engine_set_unit(gs_engine *eng, int64_t id, const double *xyz, const double *hab,
+                             const double *theta);
+
+/* One multi-signal iteration on a HOST batch (m x 3 float64): H2D, find
+ * winners against the pre-batch snapshot, winner-lock resolution, batch-order
+ * update, convergence check, stats D2H.  Synchronous. */
+gs_status gs_engine_step(gs_engine *eng, const double *signals, int64_t m, gs_batch_stats *out);
+/* Same on a DEVICE batch; asynchronous on the engine stream.  Stats land in
+ * the engine's pinned stats block; read them with gs_engine_stats. */
+gs_status gs_engine_step_device(gs_engine *eng, const double *d_signals, int64_t m);
+/* Find only: writes device winner records for signals [lo, hi) of a device
+ * batch (a multi-GPU shard), then gs_engine_update_device applies the full
+ * batch's records (after an all-gather). Records are 32 bytes per signal:
+ * int32 row1, int32 row2, float64 d2_1, float64 d2_2, 8 bytes padding. */
+gs_status gs_engine_find_device(gs_engine *eng, const double *d_signals, int64_t lo, int64_t hi,
+                                void *d_records);
+gs_status gs_engine_update_device(gs_engine *eng, const double *d_signals, int64_t m,
+                                  const void *d_records);
+/* resolve_and_update with caller-supplied winners (multi.py:99-131): winner /
+ * second ids and d_winner per signal (e.g. from an external executor).
+ * Synchronous; out receives the batch stats. */
+gs_status gs_engine_resolve_host(gs_engine *eng, const double *signals, int64_t m,
+                                 const int64_t *win_b, const int64_t *win_s,
+                                 const double *d_win, gs_batch_stats *out);
+/* Per-phase device time (CUDA events on the engine stream) accumulated over
+ * synchronous steps: out[0] find ms, out[1] update ms.  enable: 1 on, 0 off,
+ * -1 leave unchanged. */
+gs_status gs_engine_phase_ms(gs_engine *eng, int enable, double out[2]);
+/* Replace the run parameters used by subsequent updates (EngineParams). */
+gs_status gs_engine_set_params(gs_engine *eng, const gs_params *params);
+/* Synchronise the engine stream and copy out the last batch's stats. */
+gs_status gs_engine_stats(gs_engine *eng, gs_batch_stats *out);
+/* The engine's CUDA stream (cudaStream_t) for callers sharing it. */
+void *gs_engine_stream(gs_engine *eng);
+/* Pre-size device storage for ids [0, n) (avoids growth inside timed loops). */
+gs_status gs_engine_reserve(gs_engine *eng, int64_t n);
+/* Device launches issued by the engine so far (kernel count evidence). */
+int64_t gs_engine_launch_count(const gs_engine *eng);
+
+/* Counters: units, edges, next_id, tick, next_sweep, isolated, disk, half,
+ * inconsistent, untrained (hab >= h_t), rows (find rows incl. dead). */
+gs_status gs_engine_counts(gs_engine *eng, int64_t out[11]);
+/* Live units in id order: ids, positions (n x 3), hab, theta, ring class
+ * (0 disk, 1 half-disk, 2 inconsistent), patience, last_active (-1 absent). */
+gs_status gs_engine_export_units(gs_engine *eng, int64_t cap, int64_t *ids, double *pos,
+                                 double *hab, double *theta, int64_t *ring, int64_t *patience,
+                                 int64_t *last_active, int64_t *n_out);
+/* All edges (a, b, age), a < b, sorted (network.py:152-161). */
+gs_status gs_engine_export_edges(gs_engine *eng, int64_t cap, int64_t *abage, int64_t *n_out);
+/* Device audit (Network.audit, network.py:485-526): recomputes rings, degree
+ * symmetry, counters; returns the number of violations found. */
+gs_status gs_engine_audit(gs_engine *eng, int64_t *violations);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GROWSURF_B200_H */

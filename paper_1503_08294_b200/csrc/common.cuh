@@ -1,0 +1,174 @@
+// common.cuh -- shared helpers for the growsurf B200 library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+
+#include "growsurf_b200.h"
+
+// ---------------------------------------------------------------------------
+// error plumbing: every C entry point returns gs_status and records a
+// thread-local message retrievable with gs_last_error().
+
+namespace gs {
+
+void set_error(const std::string& msg);
+
+struct Fail {
+  gs_status code;
+};
+
+#define GS_CUDA(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      ::gs::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));               \
+      throw ::gs::Fail{GS_CUDA_ERROR};                                                   \
+    }                                                                                    \
+  } while (0)
+
+#define GS_CHECK(cond, code, msg)     \
+  do {                                \
+    if (!(cond)) {                    \
+      ::gs::set_error(msg);           \
+      throw ::gs::Fail{code};         \
+    }                                 \
+  } while (0)
+
+// Run a body and translate exceptions into a gs_status.
+template <class F>
+gs_status guarded(F&& f) {
+  try {
+    f();
+    return GS_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GS_CUDA_ERROR;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// IEEE binary64 arithmetic with one rounding per written operation and no
+// contraction: the reference compiles with -ffp-contract=off
+// (pkg/setup.py:38-40) and numpy never fuses.  The explicit _rn intrinsics
+// keep nvcc from forming DFMA regardless of -fmad.
+
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+// ((dx*dx + dy*dy) + dz*dz) with dx = p - s (_scan.pyx:82-85)
+__device__ __forceinline__ double dist2_exact(double px, double py, double pz, double sx,
+                                              double sy, double sz) {
+  const double dx = dsub(px, sx), dy = dsub(py, sy), dz = dsub(pz, sz);
+  return dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+}
+
+// strict-< best-two update (_scan.pyx:86-93): the incumbent keeps ties, so
+// feeding candidates in increasing row order yields lexicographic (d, row).
+struct Best2 {
+  double d1, d2;
+  int32_t i1, i2;
+  __device__ __forceinline__ void init() {
+    d1 = d2 = __longlong_as_double(0x7ff0000000000000LL);
+    i1 = i2 = -1;
+  }
+  __device__ __forceinline__ void push(double d, int32_t i) {
+    if (d < d1) {
+      d2 = d1;
+      i2 = i1;
+      d1 = d;
+      i1 = i;
+    } else if (d < d2) {
+      d2 = d;
+      i2 = i;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// growable device buffer (never shrinks; contents not preserved on growth)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) GS_CUDA(cudaFree(p));
+      p = nullptr;
+      cap = bytes + bytes / 2 + 256;
+      GS_CUDA(cudaMalloc(&p, cap));
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// context
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  // growable scratch for the host-buffer kernel-backend calls
+  void* d_buf = nullptr;
+  size_t d_cap = 0;
+  void* h_buf = nullptr;  // pinned staging
+  size_t h_cap = 0;
+  DevBuf find_work;  // split-n partials / filter candidates
+  // find-filter fallback counter (device int)
+  unsigned long long* d_fallbacks = nullptr;
+  void* ensure_device(size_t bytes);
+  void* ensure_host(size_t bytes);
+};
+
+// kernel launch counter (evidence for bench.py's gpu_launches)
+extern unsigned long long g_launches;
+
+}  // namespace gs
+
+struct gs_ctx : gs::Ctx {};
+
+// ---------------------------------------------------------------------------
+// find-winners entry points shared by the backend protocol and the engine
+
+namespace gs {
+
+// Rows are read through `rows` (row -> slot) when non-null; slots whose
+// `alive` byte is 0 are skipped.  Output forms:
+//   out_rows_d2: (m x 2) int64 rows + (m x 2) f64 squared distances
+//   out_win:     per-signal {int32 id1, int32 id2, f64 sqrt(d2_1)}
+struct WinRec {
+  int32_t b, s;
+  double dwin;
+};
+
+struct FindArgs {
+  const double* pos = nullptr;   // plain rows: n x 3 f64
+  const double4* pos4 = nullptr; // engine slots: double4 (x, y, z, -)
+  const int32_t* rows = nullptr; // engine: row -> slot
+  const uint8_t* alive = nullptr;
+  int64_t n = 0;                 // rows to scan (host value / upper bound)
+  const int* n_dev = nullptr;    // if set: exact row count read on the device
+  const double* sig = nullptr;   // m x 3 f64
+  int64_t m = 0;
+  int64_t* out_idx = nullptr;
+  double* out_d2 = nullptr;
+  WinRec* out_win = nullptr;
+  int mode = GS_FIND_AUTO;
+};
+
+void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
+
+}  // namespace gs

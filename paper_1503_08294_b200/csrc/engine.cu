@@ -1,0 +1,1764 @@
+// engine.cu -- device-resident multi-signal growing network (sm_100a).
+//
+// One multi-signal iteration (reference run_multi, pkg/src/growsurf/multi.py:134-202):
+//   find winners against the pre-batch snapshot (find.cu)
+//   -> winner-lock resolution + batch-order update (multi.py:99-131,
+//      engine.py:283-355)  [k_update_batch below]
+//   -> convergence check (engine.py:358-365).
+//
+// State layout (HBM, indexed by unit id == slot; ids are never reused,
+// network.py:10): double4 positions (32 B aligned), f64 habituation and
+// threshold, byte alive/ring flags, a fixed-capacity adjacency of
+// kMaxDeg (neighbour id, edge id) pairs per unit, and per-edge int32 ages.
+// "Rows" (the id-ordered snapshot the find scans, network.py:47-59) are an
+// append-only row->id list; dead rows are skipped by the find and compacted
+// away once they exceed 1/8 of the list.
+//
+// Update = "windowed segmented replay".  The reference applies updates one
+// signal at a time.  Within a window of up to 1024 signals, as long as the
+// topology does not change, the sequential result is a pure function of
+// per-unit event sequences: every unit wins at most once per batch (the
+// winner lock), each update touches only the winner and its neighbours, and
+// positions / habituation / edge ages evolve per unit (per edge) in batch
+// order.  So one thread per signal:
+//   A. marks candidates (alive winner and second, winner not yet claimed);
+//      the first candidate per winner is the processed signal;
+//   B. evaluates, against the window-start state, whether its update would
+//      change the topology or the sweep clock: a new b-s edge, an insertion
+//      (d_winner > theta_b and h_b(t) < h_t, with h_b(t) reconstructed from
+//      the earlier same-window decays), an edge crossing max_age, a pending
+//      sweep, or isolated units waiting for prune.  The first such signal j*
+//      is the "event";
+//   C. commits every processed signal before j* in parallel: for each
+//      touched unit the owner thread replays that unit's (signal, rate)
+//      sequence in batch order with the exact binary64 rounding sequence;
+//      each touched edge's age is replayed by the later of its two touching
+//      signals; threshold patience / shrink (engine.py:208-265) is evaluated
+//      from the reconstructed per-unit habituation at time j;
+//   D. executes j* exactly as update_single on one thread (block-parallel
+//      sweep scan), then restarts the window at j*+1.
+// Results are bit-identical to the reference's sequential loop (tests
+// compare with the C oracle and the reference golden traces).
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gs {
+
+constexpr int kMaxDeg = 64;  // adjacency slots per unit (overflow -> loud error)
+constexpr int32_t kNone32 = 0x7f7f7f7f;
+constexpr long long kNone64 = 0x7f7f7f7f7f7f7f7fLL;
+constexpr int kRingDisk = 0, kRingHalf = 1, kRingInc = 2;
+constexpr int kUpdThreads = 1024;
+constexpr long long kSweepEvery = 1024;  // engine.py:98
+constexpr int kAffCap = kMaxDeg * (kMaxDeg + 2) + 64;
+
+enum DevError {
+  E_NONE = 0,
+  E_DEGREE = 1,
+  E_UNIT_CAP = 2,
+  E_EDGE_CAP = 3,
+  E_STALE = 4,
+  E_UNKNOWN = 5,
+  E_SELF = 6,
+  E_NOEDGE = 7,
+  E_AFF = 8,
+  E_BADPOS = 9,
+};
+
+struct Counters {
+  long long tick, next_sweep;
+  long long processed, discarded, events, windows;
+  int n_units, next_id, n_edges;
+  int nrows, ndead_rows;
+  int ring_counts[3];
+  int untrained;
+  int efree_top;
+  int iso_count;
+  int error;
+  int max_degree;
+  int inserted_start;
+  int stale_n;
+  int converged;
+};
+
+struct Params {
+  double eps_b, eps_n, c_b, c_n, h_t, rho;
+  long long max_age, ring_patience, stale_factor;
+  int allow_boundary;
+};
+
+struct DevState {
+  double4* pos;
+  double* hab;
+  double* theta;
+  uint8_t* alive;
+  uint8_t* ring;
+  int32_t* deg;
+  int2* adj;  // [U * kMaxDeg] (neighbour id, edge id)
+  int32_t* patience;
+  long long* la_val;    // last_active tick, -1 when absent (engine.py:117)
+  long long* la_stamp;  // dict insertion order (3*tick + role), kNone64 when absent
+  int32_t* claim;       // batch number that claimed the unit (multi.py:114-130)
+  int32_t* firstwin;    // window scratch: first candidate signal per winner
+  int32_t* touchfirst;  // window scratch: owner signal per touched unit
+  int32_t* iso_pos;     // index in iso_list or -1
+  int32_t* rows;        // row -> id (append-only, id order)
+  int32_t* eage;        // [EC]
+  int32_t* efree;       // [EC] free edge-id stack
+  int32_t* iso_list;    // isolated units (network.py:93 _isolated)
+  long long* scratch;   // [2U] sweep (stamp, id) pairs / lonely ids
+  int32_t* aff;         // [kAffCap] ring-recompute set
+  Counters* cnt;
+  gs_batch_stats* stats;
+  int U, EC;
+};
+
+// ---------------------------------------------------------------------------
+// serial primitives (one thread).  Reference: network.py.
+
+__device__ __forceinline__ void set_err(const DevState& S, int e) {
+  if (S.cnt->error == 0) S.cnt->error = e;
+}
+
+__device__ __forceinline__ void set_hab(const DevState& S, const Params& P, int u, double h) {
+  const double old = S.hab[u];
+  if (old >= P.h_t && h < P.h_t) S.cnt->untrained--;
+  else if (old < P.h_t && h >= P.h_t) S.cnt->untrained++;
+  S.hab[u] = h;
+}
+
+__device__ void iso_add(const DevState& S, int u) {
+  Counters* c = S.cnt;
+  const int k = c->iso_count;
+  S.iso_list[k] = u;
+  S.iso_pos[u] = k;
+  c->iso_count = k + 1;
+}
+
+__device__ void iso_del(const DevState& S, int u) {
+  Counters* c = S.cnt;
+  const int k = S.iso_pos[u];
+  if (k < 0) return;
+  const int last = --c->iso_count;
+  const int w = S.iso_list[last];
+  S.iso_list[k] = w;
+  S.iso_pos[w] = k;
+  S.iso_pos[u] = -1;
+}
+
+__device__ __forceinline__ int find_slot(const DevState& S, int a, int b) {
+  const int d = S.deg[a];
+  const int2* A = S.adj + (size_t)a * kMaxDeg;
+  for (int k = 0; k < d; ++k)
+    if (A[k].x == b) return k;
+  return -1;
+}
+
+__device__ __forceinline__ int index_in(const int2* A, int k, int w) {
+  for (int i = 0; i < k; ++i)
+    if (A[i].x == w) return i;
+  return -1;
+}
+
+// _classify_ring: network.py:379-414
+__device__ int classify_ring(const DevState& S, int u) {
+  const int k = S.deg[u];
+  if (k < 2) return kRingInc;
+  const int2* A = S.adj + (size_t)u * kMaxDeg;
+  int deg1 = 0, deg2 = 0;
+  for (int a = 0; a < k; ++a) {
+    const int v = A[a].x;
+    const int dv = S.deg[v];
+    const int2* V = S.adj + (size_t)v * kMaxDeg;
+    int d = 0;
+    for (int c = 0; c < dv; ++c) {
+      if (index_in(A, k, V[c].x) >= 0) {
+        if (++d > 2) return kRingInc;
+      }
+    }
+    if (d == 1) deg1++;
+    else if (d == 2) deg2++;
+    else return kRingInc;
+  }
+  int shape;
+  if (deg1 == 0 && deg2 == k && k >= 3) shape = kRingDisk;
+  else if (deg1 == 2 && deg1 + deg2 == k) shape = kRingHalf;
+  else return kRingInc;
+  unsigned long long seen = 1ull, todo = 1ull;
+  while (todo) {
+    const int a = __ffsll((long long)todo) - 1;
+    todo &= ~(1ull << a);
+    const int v = A[a].x;
+    const int dv = S.deg[v];
+    const int2* V = S.adj + (size_t)v * kMaxDeg;
+    for (int c = 0; c < dv; ++c) {
+      const int idx = index_in(A, k, V[c].x);
+      if (idx >= 0 && !((seen >> idx) & 1ull)) {
+        seen |= 1ull << idx;
+        todo |= 1ull << idx;
+      }
+    }
+  }
+  return __popcll(seen) == k ? shape : kRingInc;
+}
+
+// _recompute_ring: network.py:416-422
+__device__ void recompute_ring(const DevState& S, int u) {
+  const int nw = classify_ring(S, u);
+  const int old = S.ring[u];
+  if (nw != old) {
+    S.ring[u] = (uint8_t)nw;
+    S.cnt->ring_counts[old]--;
+    S.cnt->ring_counts[nw]++;
+  }
+}
+
+// _ring_neighborhood: network.py:424-433 -> appended to out; returns count
+__device__ int ring_neighborhood(const DevState& S, int a, int b, int32_t* out, int room) {
+  int n = 0;
+  const int da = S.deg[a];
+  const int2* A = S.adj + (size_t)a * kMaxDeg;
+  if (room < da + 2) {
+    set_err(S, E_AFF);
+    return 0;
+  }
+  for (int k = 0; k < da; ++k) {
+    const int v = A[k].x;
+    if (v != b && find_slot(S, b, v) >= 0) out[n++] = v;
+  }
+  out[n++] = a;
+  out[n++] = b;
+  return n;
+}
+
+// add_unit: network.py:208-230
+__device__ int add_unit(const DevState& S, const Params& P, double x, double y, double z,
+                        double threshold) {
+  Counters* c = S.cnt;
+  if (!(isfinite(x) && isfinite(y) && isfinite(z)) || !(isfinite(threshold) && threshold > 0.0)) {
+    set_err(S, E_BADPOS);
+    return -1;
+  }
+  const int id = c->next_id;
+  if (id >= S.U) {
+    set_err(S, E_UNIT_CAP);
+    return -1;
+  }
+  c->next_id = id + 1;
+  S.pos[id] = make_double4(x, y, z, 0.0);
+  S.hab[id] = 1.0;
+  S.theta[id] = threshold;
+  S.alive[id] = 1;
+  S.ring[id] = kRingInc;
+  c->ring_counts[kRingInc]++;
+  S.deg[id] = 0;
+  S.patience[id] = 0;
+  S.la_val[id] = -1;
+  S.la_stamp[id] = kNone64;
+  S.claim[id] = -1;
+  S.firstwin[id] = kNone32;
+  S.touchfirst[id] = kNone32;
+  iso_add(S, id);
+  c->n_units++;
+  if (1.0 >= P.h_t) c->untrained++;
+  S.rows[c->nrows++] = id;
+  return id;
+}
+
+// _remove_edge_raw: network.py:453-462
+__device__ void remove_edge_raw(const DevState& S, int a, int b) {
+  Counters* c = S.cnt;
+  const int ka = find_slot(S, a, b);
+  if (ka < 0) {
+    set_err(S, E_NOEDGE);
+    return;
+  }
+  int2* A = S.adj + (size_t)a * kMaxDeg;
+  int2* B = S.adj + (size_t)b * kMaxDeg;
+  const int e = A[ka].y;
+  const int da = --S.deg[a];
+  A[ka] = A[da];
+  const int kb = find_slot(S, b, a);
+  const int db = --S.deg[b];
+  B[kb] = B[db];
+  S.efree[c->efree_top++] = e;
+  c->n_edges--;
+  if (da == 0) iso_add(S, a);
+  if (db == 0) iso_add(S, b);
+}
+
+// _remove_unit_raw: network.py:464-480 (precondition: no edges)
+__device__ void remove_unit_raw(const DevState& S, const Params& P, int u) {
+  Counters* c = S.cnt;
+  S.alive[u] = 0;
+  c->n_units--;
+  c->ring_counts[S.ring[u]]--;
+  iso_del(S, u);
+  if (S.hab[u] >= P.h_t) c->untrained--;
+  c->ndead_rows++;
+}
+
+// remove_unit: network.py:232-240
+__device__ void remove_unit(const DevState& S, const Params& P, int u) {
+  int nb[kMaxDeg];
+  const int k = S.deg[u];
+  const int2* U_ = S.adj + (size_t)u * kMaxDeg;
+  for (int i = 0; i < k; ++i) nb[i] = U_[i].x;
+  for (int i = 0; i < k; ++i) remove_edge_raw(S, u, nb[i]);
+  remove_unit_raw(S, P, u);
+  for (int i = 0; i < k; ++i) recompute_ring(S, nb[i]);
+}
+
+// connect_or_reset: network.py:261-282.  1 created, 0 reset, -1 error.
+__device__ int connect_or_reset(const DevState& S, int a, int b) {
+  Counters* c = S.cnt;
+  const int k = find_slot(S, a, b);
+  if (k >= 0) {
+    S.eage[S.adj[(size_t)a * kMaxDeg + k].y] = 0;
+    return 0;
+  }
+  if (S.deg[a] >= kMaxDeg || S.deg[b] >= kMaxDeg) {
+    set_err(S, E_DEGREE);
+    return -1;
+  }
+  if (c->efree_top <= 0) {
+    set_err(S, E_EDGE_CAP);
+    return -1;
+  }
+  const int e = S.efree[--c->efree_top];
+  S.eage[e] = 0;
+  if (S.deg[a] == 0) iso_del(S, a);
+  if (S.deg[b] == 0) iso_del(S, b);
+  S.adj[(size_t)a * kMaxDeg + S.deg[a]++] = make_int2(b, e);
+  S.adj[(size_t)b * kMaxDeg + S.deg[b]++] = make_int2(a, e);
+  c->n_edges++;
+  const int dm = max(S.deg[a], S.deg[b]);
+  if (dm > c->max_degree) c->max_degree = dm;
+  const int n = ring_neighborhood(S, a, b, S.aff, kAffCap);
+  for (int i = 0; i < n; ++i) recompute_ring(S, S.aff[i]);
+  return 1;
+}
+
+// remove_edge: network.py:284-292
+__device__ void remove_edge(const DevState& S, int a, int b) {
+  const int n = ring_neighborhood(S, a, b, S.aff, kAffCap);
+  remove_edge_raw(S, a, b);
+  for (int i = 0; i < n; ++i) recompute_ring(S, S.aff[i]);
+}
+
+// age_incident_edges(b, inc, exclude): network.py:294-319.  Records the
+// neighbours whose shared edge crossed max_age (the over-age registry,
+// network.py:315-316; it only ever holds edges of the current winner).
+__device__ int age_incident(const DevState& S, const Params& P, int b, int exclude, int inc,
+                            int32_t* over, int* nover) {
+  const int d = S.deg[b];
+  const int2* B = S.adj + (size_t)b * kMaxDeg;
+  int top = 0;
+  for (int k = 0; k < d; ++k) {
+    const int v = B[k].x;
+    if (v == exclude) continue;
+    const int e = B[k].y;
+    const int old = S.eage[e];
+    const int nw = old + inc;
+    S.eage[e] = nw;
+    if (nw > top) top = nw;
+    if (over && nw > P.max_age && old <= P.max_age) over[(*nover)++] = v;
+  }
+  return top;
+}
+
+__device__ void sort_ll(long long* a, int n) {  // insertion sort (small n)
+  for (int i = 1; i < n; ++i) {
+    const long long x = a[i];
+    int j = i - 1;
+    while (j >= 0 && a[j] > x) {
+      a[j + 1] = a[j];
+      --j;
+    }
+    a[j + 1] = x;
+  }
+}
+
+// removes isolated units in ascending id order down to a floor of 2 units
+// (network.py:355-365); returns how many were removed
+__device__ int remove_lonely(const DevState& S, const Params& P) {
+  Counters* c = S.cnt;
+  const int n = c->iso_count;
+  if (n == 0) return 0;
+  long long* ids = S.scratch;
+  for (int i = 0; i < n; ++i) ids[i] = S.iso_list[i];
+  sort_ll(ids, n);
+  int removed = 0;
+  for (int i = 0; i < n; ++i) {
+    if (c->n_units <= 2) break;
+    remove_unit_raw(S, P, (int)ids[i]);
+    removed++;
+  }
+  return removed;
+}
+
+// prune on the winner's over-age edges: network.py:321-369.  The removal
+// order of the over-age edges cannot change the result (ring classes are a
+// function of the final adjacency and every ring that can change is in the
+// union of the ring neighbourhoods); lonely units go in ascending id order.
+__device__ void prune_winner(const DevState& S, const Params& P, int b, const int32_t* over,
+                             int nover, int* pe, int* pu) {
+  *pe = 0;
+  *pu = 0;
+  if (nover == 0 && S.cnt->iso_count == 0) return;
+  int naff = 0;
+  for (int i = 0; i < nover; ++i) {
+    naff += ring_neighborhood(S, b, over[i], S.aff + naff, kAffCap - naff);
+    remove_edge_raw(S, b, over[i]);
+  }
+  *pu = remove_lonely(S, P);
+  for (int i = 0; i < naff; ++i)
+    if (S.alive[S.aff[i]]) recompute_ring(S, S.aff[i]);
+  *pe = nover;
+}
+
+// generic prune(max_age) for the Network API (scans every edge)
+__device__ void prune_all(const DevState& S, const Params& P, long long max_age, int* pe,
+                          int* pu) {
+  Counters* c = S.cnt;
+  int npe = 0;
+  for (int a = 0; a < c->next_id; ++a) {
+    if (!S.alive[a]) continue;
+    for (int k = 0; k < S.deg[a];) {
+      const int2 ent = S.adj[(size_t)a * kMaxDeg + k];
+      if (a < ent.x && S.eage[ent.y] > max_age) {
+        int nb[kMaxDeg + 2];
+        // ring_neighborhood into a local list, then remove
+        int n = 0;
+        const int da = S.deg[a];
+        for (int q = 0; q < da; ++q) {
+          const int v = S.adj[(size_t)a * kMaxDeg + q].x;
+          if (v != ent.x && find_slot(S, ent.x, v) >= 0 && n < kMaxDeg) nb[n++] = v;
+        }
+        nb[n++] = a;
+        nb[n++] = ent.x;
+        remove_edge_raw(S, a, ent.x);
+        for (int q = 0; q < n; ++q)
+          if (S.alive[nb[q]]) recompute_ring(S, nb[q]);
+        npe++;
+        continue;  // slot k now holds a different entry
+      }
+      ++k;
+    }
+  }
+  *pu = remove_lonely(S, P);
+  *pe = npe;
+}
+
+// last_active[u] = tick (engine.py:305-306,339) with dict order stamps
+__device__ __forceinline__ void touch_active(const DevState& S, int u, long long tick, int role) {
+  if (S.la_val[u] == -1) S.la_stamp[u] = 3 * tick + role;
+  S.la_val[u] = tick;
+}
+
+// _sweep_stale body over a collected (stamp, id) list: engine.py:268-280
+__device__ void sweep_apply(const DevState& S, const Params& P, long long* rec, int n) {
+  // sort by stamp (dict iteration order)
+  for (int i = 1; i < n; ++i) {
+    const long long ks = rec[2 * i], kid = rec[2 * i + 1];
+    int j = i - 1;
+    while (j >= 0 && rec[2 * j] > ks) {
+      rec[2 * (j + 1)] = rec[2 * j];
+      rec[2 * (j + 1) + 1] = rec[2 * j + 1];
+      --j;
+    }
+    rec[2 * (j + 1)] = ks;
+    rec[2 * (j + 1) + 1] = kid;
+  }
+  for (int i = 0; i < n; ++i) {
+    const int u = (int)rec[2 * i + 1];
+    S.la_val[u] = -1;
+    S.la_stamp[u] = kNone64;
+    S.patience[u] = 0;
+    if (S.alive[u] && S.cnt->n_units > 2) remove_unit(S, P, u);
+  }
+}
+
+__device__ __forceinline__ long long sweep_cutoff(const DevState& S, const Params& P) {
+  const long long v = S.cnt->n_units;
+  return S.cnt->tick - P.stale_factor * (v > 100 ? v : 100);
+}
+
+// adapt_threshold: engine.py:208-238
+__device__ void adapt_threshold(const DevState& S, const Params& P, int b) {
+  const int ring = S.ring[b];
+  if (ring == kRingDisk || (P.allow_boundary && ring == kRingHalf)) {
+    S.patience[b] = 0;
+    return;
+  }
+  if (S.hab[b] >= P.h_t) return;
+  const int d = S.deg[b];
+  const int2* B = S.adj + (size_t)b * kMaxDeg;
+  for (int k = 0; k < d; ++k)
+    if (S.hab[B[k].x] >= P.h_t) return;
+  int count = S.patience[b] + 1;
+  if (count >= P.ring_patience) {
+    S.theta[b] = dmul(S.theta[b], P.rho);
+    count = 0;
+  }
+  S.patience[b] = count;
+}
+
+__device__ __forceinline__ void move_toward(double4& p, double eps, double x, double y, double z) {
+  p.x = dadd(p.x, dmul(eps, dsub(x, p.x)));
+  p.y = dadd(p.y, dmul(eps, dsub(y, p.y)));
+  p.z = dadd(p.z, dmul(eps, dsub(z, p.z)));
+}
+
+// update_single, everything up to and including prune (engine.py:297-344).
+// Returns 1 if the sweep clock fired (engine.py:346).
+__device__ int serial_update_part1(const DevState& S, const Params& P, int b, int s, double dw,
+                                   double x, double y, double z) {
+  Counters* c = S.cnt;
+  const long long tick = ++c->tick;
+  touch_active(S, b, tick, 0);
+  touch_active(S, s, tick, 1);
+  if (connect_or_reset(S, b, s) < 0) return 0;
+  int32_t over[kMaxDeg];
+  int nover = 0;
+  age_incident(S, P, b, s, 1, over, &nover);
+  double4 wp = S.pos[b];
+  move_toward(wp, P.eps_b, x, y, z);
+  S.pos[b] = wp;
+  set_hab(S, P, b, dmul(S.hab[b], P.c_b));
+  {
+    const int d = S.deg[b];
+    const int2* B = S.adj + (size_t)b * kMaxDeg;
+    for (int k = 0; k < d; ++k) {
+      const int v = B[k].x;
+      double4 pv = S.pos[v];
+      move_toward(pv, P.eps_n, x, y, z);
+      S.pos[v] = pv;
+      set_hab(S, P, v, dmul(S.hab[v], P.c_n));
+    }
+  }
+  // maybe_insert: engine.py:184-205 gated at :336
+  if (dw > S.theta[b] && S.hab[b] < P.h_t) {
+    const double theta_b = S.theta[b];
+    const double mx = dmul(dadd(wp.x, x), 0.5);
+    const double my = dmul(dadd(wp.y, y), 0.5);
+    const double mz = dmul(dadd(wp.z, z), 0.5);
+    const int r = add_unit(S, P, mx, my, mz, theta_b);
+    if (r < 0) return 0;
+    connect_or_reset(S, r, b);
+    connect_or_reset(S, r, s);
+    if (find_slot(S, b, s) >= 0) remove_edge(S, b, s);
+    touch_active(S, r, tick, 2);
+  }
+  int pe, pu;
+  prune_winner(S, P, b, over, nover, &pe, &pu);
+  return tick >= c->next_sweep ? 1 : 0;
+}
+
+// sweep bookkeeping + adapt_threshold (engine.py:345-355)
+__device__ void serial_update_part2(const DevState& S, const Params& P, int b, int swept_n,
+                                    bool sweep_fired) {
+  Counters* c = S.cnt;
+  if (sweep_fired) {
+    if (swept_n > 0) sweep_apply(S, P, S.scratch, swept_n);
+    c->next_sweep = c->tick + kSweepEvery;
+  }
+  if (S.alive[b]) adapt_threshold(S, P, b);
+}
+
+// single-thread stale collection (API path)
+__device__ int collect_stale_serial(const DevState& S, const Params& P) {
+  const long long cutoff = sweep_cutoff(S, P);
+  if (cutoff <= 0) return 0;
+  int n = 0;
+  for (int u = 0; u < S.cnt->next_id; ++u)
+    if (S.la_val[u] != -1 && S.la_val[u] < cutoff) {
+      S.scratch[2 * n] = S.la_stamp[u];
+      S.scratch[2 * n + 1] = u;
+      ++n;
+    }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// block primitives (1024 threads)
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// exclusive scan across the block; *total = block sum.  Contains __syncthreads.
+__device__ int block_excl_scan(int v, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int inc = warp_incl_scan(v);
+  __syncthreads();
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int x = lane < nw ? s_warp[lane] : 0;
+    const int xi = warp_incl_scan(x);
+    if (lane < nw) s_warp[lane] = xi - x;
+    if (lane == 31) s_warp[32] = xi;
+  }
+  __syncthreads();
+  *total = s_warp[32];
+  return s_warp[wid] + inc - v;
+}
+
+__device__ int block_min(int v, int* s_warp) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) s_warp[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    int x = lane < nw ? s_warp[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) s_warp[32] = x;
+  }
+  __syncthreads();
+  return s_warp[32];
+}
+
+__device__ int block_sum(int v, int* s_warp) {
+  int total;
+  block_excl_scan(v, s_warp, &total);
+  return total;
+}
+
+// ---------------------------------------------------------------------------
+// window helpers
+
+// replay unit u's updates from this window's committed signals in batch
+// order (the exact per-unit rounding sequence of the sequential loop)
+__device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
+                          int jstar) {
+  const int2* A = S.adj + (size_t)u * kMaxDeg;
+  const int d = S.deg[u];
+  const int jself = S.firstwin[u];
+  double4 p = S.pos[u];
+  const double h0 = S.hab[u];
+  double h = h0;
+  int cur = -1;
+  while (true) {
+    int nxt = 0x7fffffff;
+    bool self = false;
+    if (jself < jstar && jself > cur) {
+      nxt = jself;
+      self = true;
+    }
+    for (int k = 0; k < d; ++k) {
+      const int jw = S.firstwin[A[k].x];
+      if (jw < jstar && jw > cur && jw < nxt) {
+        nxt = jw;
+        self = false;
+      }
+    }
+    if (nxt == 0x7fffffff) break;
+    cur = nxt;
+    const double x = sig[3 * (size_t)nxt], y = sig[3 * (size_t)nxt + 1], z = sig[3 * (size_t)nxt + 2];
+    if (self) {
+      move_toward(p, P.eps_b, x, y, z);
+      h = dmul(h, P.c_b);
+    } else {
+      move_toward(p, P.eps_n, x, y, z);
+      h = dmul(h, P.c_n);
+    }
+  }
+  S.pos[u] = p;
+  S.hab[u] = h;
+  if (h0 >= P.h_t && h < P.h_t) atomicSub(&S.cnt->untrained, 1);
+}
+
+__device__ __forceinline__ double pow_chain(double h, double c, int k) {
+  for (int i = 0; i < k; ++i) h = dmul(h, c);
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// the batch update kernel: one CTA of 1024 threads
+
+__global__ void __launch_bounds__(kUpdThreads, 1)
+    k_update_batch(DevState S, Params P, const double* __restrict__ sig,
+                   const WinRec* __restrict__ rec, int m, int batch_no) {
+  __shared__ int s_warp[33];
+  __shared__ int s_i[4];
+  __shared__ long long s_ll[2];
+  Counters* c = S.cnt;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    c->processed = c->discarded = c->events = c->windows = 0;
+    c->inserted_start = c->next_id;
+    c->stale_n = 0;
+  }
+  __syncthreads();
+  int j0 = 0;
+  while (j0 < m) {
+    const int j = j0 + tid;
+    const bool act = j < m;
+    const int next_id = c->next_id;
+    int b = -1, s = -1;
+    double dw = 0.0;
+    bool cand = false;
+    if (act) {
+      const WinRec r = rec[j];
+      b = r.b;
+      s = r.s;
+      dw = r.dwin;
+      cand = b >= 0 && s >= 0 && b < next_id && s < next_id && b != s && S.alive[b] &&
+             S.alive[s] && S.claim[b] != batch_no;
+    }
+    if (cand) atomicMin(&S.firstwin[b], j);
+    __syncthreads();
+    const bool proc = cand && S.firstwin[b] == j;
+    int nproc;
+    const int rank = block_excl_scan(proc ? 1 : 0, s_warp, &nproc);
+    const long long tick_j = c->tick + rank + 1;
+    bool ev = false;
+    int newpat = -2;
+    bool shrink = false;
+    bool absent_b = false, absent_s = false;
+    if (proc) {
+      ev = c->iso_count > 0 || tick_j >= c->next_sweep;
+      const int db = S.deg[b];
+      const int2* B = S.adj + (size_t)b * kMaxDeg;
+      bool found = false;
+      int kcn = 0;
+      for (int k = 0; k < db; ++k) {
+        const int2 ent = B[k];
+        const int v = ent.x;
+        const int jv = S.firstwin[v];
+        if (v == s) found = true;
+        if (jv < j) kcn++;
+        if (v != s) {
+          int age = S.eage[ent.y];
+          if (jv < j) age = (rec[jv].s == b) ? 0 : age + 1;
+          if (age + 1 > P.max_age) ev = true;
+        }
+      }
+      if (!found) ev = true;  // connect_or_reset would create b-s
+      const double hb = dmul(pow_chain(S.hab[b], P.c_n, kcn), P.c_b);
+      if (dw > S.theta[b] && hb < P.h_t) ev = true;  // insertion
+      if (!ev) {
+        // adapt_threshold at time j (engine.py:208-265)
+        const int ring = S.ring[b];
+        if (ring == kRingDisk || (P.allow_boundary && ring == kRingHalf)) {
+          newpat = 0;
+        } else if (hb < P.h_t) {
+          bool ok = true;
+          for (int k = 0; k < db && ok; ++k) {
+            const int v = B[k].x;
+            const int jv = S.firstwin[v];
+            const bool vwon = jv < j;
+            const int dv = S.deg[v];
+            const int2* V = S.adj + (size_t)v * kMaxDeg;
+            int k1 = 0, k2 = 0;
+            for (int q = 0; q < dv; ++q) {
+              const int jw = S.firstwin[V[q].x];
+              if (jw <= j) {
+                if (vwon && jw > jv) k2++;
+                else k1++;
+              }
+            }
+            double hv = pow_chain(S.hab[v], P.c_n, k1);
+            if (vwon) hv = dmul(hv, P.c_b);
+            hv = pow_chain(hv, P.c_n, k2);
+            if (hv >= P.h_t) ok = false;
+          }
+          if (ok) {
+            int cnt = S.patience[b] + 1;
+            if (cnt >= P.ring_patience) {
+              shrink = true;
+              cnt = 0;
+            }
+            newpat = cnt;
+          }
+        }
+      }
+      absent_b = S.la_val[b] == -1;
+      absent_s = S.la_val[s] == -1;
+    }
+    const int wend = min(j0 + kUpdThreads, m);
+    int jstar = block_min((proc && ev) ? j : 0x7fffffff, s_warp);
+    if (jstar == 0x7fffffff) jstar = wend;
+    const bool com = proc && j < jstar;
+    if (com) {
+      S.claim[b] = batch_no;
+      if (absent_b) atomicMin(&S.la_stamp[b], 3 * tick_j);
+      atomicMax(&S.la_val[b], tick_j);
+      if (absent_s) atomicMin(&S.la_stamp[s], 3 * tick_j + 1);
+      atomicMax(&S.la_val[s], tick_j);
+      atomicMin(&S.touchfirst[b], j);
+      const int db = S.deg[b];
+      const int2* B = S.adj + (size_t)b * kMaxDeg;
+      for (int k = 0; k < db; ++k) atomicMin(&S.touchfirst[B[k].x], j);
+      if (newpat != -2) {
+        S.patience[b] = newpat;
+        if (shrink) S.theta[b] = dmul(S.theta[b], P.rho);
+      }
+    }
+    __syncthreads();
+    if (com) {
+      if (S.touchfirst[b] == j) walk_unit(S, P, sig, b, jstar);
+      const int db = S.deg[b];
+      const int2* B = S.adj + (size_t)b * kMaxDeg;
+      for (int k = 0; k < db; ++k) {
+        const int2 ent = B[k];
+        const int v = ent.x;
+        if (S.touchfirst[v] == j) walk_unit(S, P, sig, v, jstar);
+        const int jv = S.firstwin[v];
+        if (jv < jstar && jv > j) continue;  // v's signal replays this edge
+        int age = S.eage[ent.y];
+        if (jv < j) age = (rec[jv].s == b) ? 0 : age + 1;
+        age = (v == s) ? 0 : age + 1;
+        S.eage[ent.y] = age;
+      }
+    }
+    const int ncom = block_sum(com ? 1 : 0, s_warp);
+    const int ndisc = block_sum((act && j < jstar && !proc) ? 1 : 0, s_warp);
+    if (tid == 0) {
+      c->tick += ncom;
+      c->processed += ncom;
+      c->discarded += ndisc;
+      c->windows++;
+    }
+    __syncthreads();
+    if (cand) S.firstwin[b] = kNone32;
+    if (com) {
+      S.touchfirst[b] = kNone32;
+      const int db = S.deg[b];
+      const int2* B = S.adj + (size_t)b * kMaxDeg;
+      for (int k = 0; k < db; ++k) S.touchfirst[B[k].x] = kNone32;
+    }
+    __syncthreads();
+    if (jstar < wend) {
+      // the event signal, executed exactly as update_single
+      if (tid == 0) {
+        const WinRec r = rec[jstar];
+        S.claim[r.b] = batch_no;
+        const int fired = serial_update_part1(S, P, r.b, r.s, r.dwin, sig[3 * (size_t)jstar],
+                                              sig[3 * (size_t)jstar + 1],
+                                              sig[3 * (size_t)jstar + 2]);
+        c->processed++;
+        c->events++;
+        c->stale_n = 0;
+        s_i[0] = fired;
+        s_ll[0] = fired ? sweep_cutoff(S, P) : 0;
+        s_i[1] = r.b;
+      }
+      __syncthreads();
+      const int fired = s_i[0];
+      const long long cutoff = s_ll[0];
+      if (fired && cutoff > 0) {
+        const int nid = c->next_id;
+        for (int u = tid; u < nid; u += kUpdThreads) {
+          const long long t = S.la_val[u];
+          if (t != -1 && t < cutoff) {
+            const int q = atomicAdd(&c->stale_n, 1);
+            S.scratch[2 * q] = S.la_stamp[u];
+            S.scratch[2 * q + 1] = u;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) serial_update_part2(S, P, s_i[1], c->stale_n, fired != 0);
+      __syncthreads();
+      j0 = jstar + 1;
+    } else {
+      j0 = wend;
+    }
+    __syncthreads();
+  }
+  // compact rows when dead entries exceed 1/8 (keeps id order)
+  if (c->ndead_rows * 8 > c->nrows) {
+    const int n = c->nrows;
+    int out = 0;
+    for (int base = 0; base < n; base += kUpdThreads) {
+      const int r = base + tid;
+      const int id = r < n ? S.rows[r] : -1;
+      const int keep = (id >= 0 && S.alive[id]) ? 1 : 0;
+      int tot;
+      const int rk = block_excl_scan(keep, s_warp, &tot);
+      if (keep) S.rows[out + rk] = id;
+      out += tot;
+      __syncthreads();
+    }
+    if (tid == 0) {
+      c->nrows = out;
+      c->ndead_rows = 0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    // is_converged: engine.py:358-365 (max(h) < h_t <=> no untrained unit)
+    int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
+    c->converged = (c->n_units >= 4 && ok == c->n_units && c->untrained == 0) ? 1 : 0;
+    gs_batch_stats* st = S.stats;
+    st->processed = c->processed;
+    st->discarded = c->discarded;
+    st->inserted = c->next_id - c->inserted_start;
+    st->units = c->n_units;
+    st->edges = c->n_edges;
+    st->next_id = c->next_id;
+    st->converged = c->converged;
+    st->tick = c->tick;
+    st->events = c->events;
+    st->windows = c->windows;
+    st->error = c->error;
+    st->max_degree = c->max_degree;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Network API operations (single thread; not on the hot path)
+
+enum OpCode {
+  OP_ADD = 1,
+  OP_CONNECT = 2,
+  OP_REMOVE_UNIT = 3,
+  OP_REMOVE_EDGE = 4,
+  OP_AGE = 5,
+  OP_PRUNE = 6,
+  OP_SET = 7,
+};
+
+struct OpArgs {
+  int op;
+  int a, b;
+  long long i0;
+  double x, y, z, t, t2;
+  int flags;  // OP_SET: 1 pos, 2 hab, 4 theta
+};
+
+__device__ bool valid_unit(const DevState& S, int u) {
+  return u >= 0 && u < S.cnt->next_id && S.alive[u];
+}
+
+__global__ void k_op(DevState S, Params P, OpArgs a, long long* res) {
+  Counters* c = S.cnt;
+  res[0] = 0;
+  res[1] = 0;
+  res[2] = 0;
+  switch (a.op) {
+    case OP_ADD: {
+      res[0] = add_unit(S, P, a.x, a.y, a.z, a.t);
+      break;
+    }
+    case OP_CONNECT: {
+      if (a.a == a.b) { res[2] = E_SELF; break; }
+      if (!valid_unit(S, a.a) || !valid_unit(S, a.b)) { res[2] = E_UNKNOWN; break; }
+      res[0] = connect_or_reset(S, a.a, a.b);
+      break;
+    }
+    case OP_REMOVE_UNIT: {
+      if (!valid_unit(S, a.a)) { res[2] = E_UNKNOWN; break; }
+      remove_unit(S, P, a.a);
+      break;
+    }
+    case OP_REMOVE_EDGE: {
+      if (!valid_unit(S, a.a) || !valid_unit(S, a.b)) { res[2] = E_UNKNOWN; break; }
+      if (find_slot(S, a.a, a.b) < 0) { res[2] = E_NOEDGE; break; }
+      remove_edge(S, a.a, a.b);
+      break;
+    }
+    case OP_AGE: {
+      if (!valid_unit(S, a.a)) { res[2] = E_UNKNOWN; break; }
+      res[0] = age_incident(S, P, a.a, a.b, (int)a.i0, nullptr, nullptr);
+      break;
+    }
+    case OP_PRUNE: {
+      int pe, pu;
+      prune_all(S, P, a.i0, &pe, &pu);
+      res[0] = pe;
+      res[1] = pu;
+      break;
+    }
+    case OP_SET: {
+      if (!valid_unit(S, a.a)) { res[2] = E_UNKNOWN; break; }
+      if (a.flags & 1) {
+        double4 p = S.pos[a.a];
+        p.x = a.x;
+        p.y = a.y;
+        p.z = a.z;
+        S.pos[a.a] = p;
+      }
+      if (a.flags & 2) set_hab(S, P, a.a, a.t);
+      if (a.flags & 4) S.theta[a.a] = a.t2;
+      break;
+    }
+  }
+  if (c->error && !res[2]) res[2] = 100 + c->error;
+}
+
+// audit (Network.audit, network.py:485-526): counts violations
+__global__ void k_audit(DevState S, Params P, unsigned long long* bad) {
+  const Counters* c = S.cnt;
+  __shared__ int s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  // 0 units, 1 edge halves, 2 isolated, 3 disk, 4 half, 5 inc, 6 untrained
+  for (int u = threadIdx.x; u < c->next_id; u += blockDim.x) {
+    if (!S.alive[u]) continue;
+    atomicAdd(&s_cnt[0], 1);
+    const int d = S.deg[u];
+    atomicAdd(&s_cnt[1], d);
+    if (d == 0) atomicAdd(&s_cnt[2], 1);
+    atomicAdd(&s_cnt[3 + S.ring[u]], 1);
+    if (S.hab[u] >= P.h_t) atomicAdd(&s_cnt[6], 1);
+    if (classify_ring(S, u) != S.ring[u]) atomicAdd(bad, 1ull);
+    if (!(S.hab[u] >= 0.0 && S.hab[u] <= 1.0) || !(S.theta[u] > 0.0)) atomicAdd(bad, 1ull);
+    for (int k = 0; k < d; ++k) {
+      const int2 ent = S.adj[(size_t)u * kMaxDeg + k];
+      const int v = ent.x;
+      if (v == u || v < 0 || v >= c->next_id || !S.alive[v]) {
+        atomicAdd(bad, 1ull);
+        continue;
+      }
+      const int kv = find_slot(S, v, u);
+      if (kv < 0 || S.adj[(size_t)v * kMaxDeg + kv].y != ent.y) atomicAdd(bad, 1ull);
+      if (S.eage[ent.y] < 0) atomicAdd(bad, 1ull);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long e = 0;
+    e += s_cnt[0] != c->n_units;
+    e += s_cnt[1] != 2 * c->n_edges;
+    e += s_cnt[2] != c->iso_count;
+    e += s_cnt[3] != c->ring_counts[0];
+    e += s_cnt[4] != c->ring_counts[1];
+    e += s_cnt[5] != c->ring_counts[2];
+    e += s_cnt[6] != c->untrained;
+    atomicAdd(bad, e);
+  }
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_fill_i64(long long* p, int64_t n, long long v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// push edge ids [lo, hi) onto the free stack, lowest id on top
+__global__ void k_push_free(int32_t* efree, int top, int lo, int hi) {
+  const int n = hi - lo;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    efree[top + i] = hi - 1 - i;
+}
+
+__global__ void k_set_top(Counters* c, int delta) { c->efree_top += delta; }
+
+}  // namespace gs
+
+using namespace gs;
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct gs_engine {
+  gs_ctx* ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  gs_params hp{};
+  Params P{};
+  DevState S{};
+  int U = 0, EC = 0;
+  DevBuf find_work;
+  DevBuf sig_buf;
+  DevBuf rec_buf;
+  gs_batch_stats* h_stats = nullptr;  // pinned
+  double* h_sig = nullptr;            // pinned staging for host batches
+  size_t h_sig_cap = 0;
+  long long* d_res = nullptr;
+  long long* h_res = nullptr;
+  int batch_no = 0;
+  long long launches = 0;
+  // optional per-phase device timing (CUDA events on the engine stream)
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  bool timing = false, ev_pending = false;
+  double find_ms = 0.0, update_ms = 0.0;
+  // host mirror of the last known counters
+  int next_id = 0, n_edges = 0, n_units = 0;
+};
+
+namespace {
+
+template <class T>
+void grow_array(T*& p, size_t old_n, size_t new_n, cudaStream_t st) {
+  T* q = nullptr;
+  GS_CUDA(cudaMalloc(&q, sizeof(T) * new_n));
+  if (p && old_n) GS_CUDA(cudaMemcpyAsync(q, p, sizeof(T) * old_n, cudaMemcpyDeviceToDevice, st));
+  if (p) {
+    GS_CUDA(cudaStreamSynchronize(st));
+    GS_CUDA(cudaFree(p));
+  }
+  p = q;
+}
+
+void fill_i32(int32_t* p, int64_t n, int32_t v, cudaStream_t st) {
+  if (n <= 0) return;
+  k_fill_i32<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(p, n, v);
+  GS_CUDA(cudaGetLastError());
+}
+
+void fill_i64(long long* p, int64_t n, long long v, cudaStream_t st) {
+  if (n <= 0) return;
+  k_fill_i64<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(p, n, v);
+  GS_CUDA(cudaGetLastError());
+}
+
+void grow_units(gs_engine* e, int new_u) {
+  if (new_u <= e->U) return;
+  const int old = e->U;
+  cudaStream_t st = e->stream;
+  DevState& S = e->S;
+  grow_array(S.pos, old, new_u, st);
+  grow_array(S.hab, old, new_u, st);
+  grow_array(S.theta, old, new_u, st);
+  grow_array(S.alive, old, new_u, st);
+  grow_array(S.ring, old, new_u, st);
+  grow_array(S.deg, old, new_u, st);
+  grow_array(S.adj, (size_t)old * kMaxDeg, (size_t)new_u * kMaxDeg, st);
+  grow_array(S.patience, old, new_u, st);
+  grow_array(S.la_val, old, new_u, st);
+  grow_array(S.la_stamp, old, new_u, st);
+  grow_array(S.claim, old, new_u, st);
+  grow_array(S.firstwin, old, new_u, st);
+  grow_array(S.touchfirst, old, new_u, st);
+  grow_array(S.iso_pos, old, new_u, st);
+  grow_array(S.rows, old, new_u, st);
+  grow_array(S.iso_list, old, new_u, st);
+  // scratch content is transient: plain reallocation
+  if (S.scratch) GS_CUDA(cudaFree(S.scratch));
+  GS_CUDA(cudaMalloc(&S.scratch, sizeof(long long) * 2 * (size_t)new_u + 64));
+  const int64_t add = new_u - old;
+  GS_CUDA(cudaMemsetAsync(S.alive + old, 0, add, st));
+  GS_CUDA(cudaMemsetAsync(S.deg + old, 0, sizeof(int32_t) * add, st));
+  fill_i32(S.firstwin + old, add, kNone32, st);
+  fill_i32(S.touchfirst + old, add, kNone32, st);
+  fill_i32(S.claim + old, add, -1, st);
+  fill_i32(S.iso_pos + old, add, -1, st);
+  fill_i64(S.la_val + old, add, -1, st);
+  fill_i64(S.la_stamp + old, add, kNone64, st);
+  e->U = new_u;
+  S.U = new_u;
+}
+
+void grow_edges(gs_engine* e, int new_ec) {
+  if (new_ec <= e->EC) return;
+  const int old = e->EC;
+  cudaStream_t st = e->stream;
+  DevState& S = e->S;
+  grow_array(S.eage, old, new_ec, st);
+  // the free stack keeps its first efree_top entries; new ids go on top of
+  // them in descending order so the lowest new id pops first
+  int32_t* nf = nullptr;
+  GS_CUDA(cudaMalloc(&nf, sizeof(int32_t) * (size_t)new_ec));
+  int top = 0;
+  if (S.efree) {
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    top = hc.efree_top;
+    // existing free ids sit below; new ids above (popped first) - order of
+    // edge ids is never observable
+    if (top) GS_CUDA(cudaMemcpyAsync(nf, S.efree, sizeof(int32_t) * top, cudaMemcpyDeviceToDevice, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    GS_CUDA(cudaFree(S.efree));
+  }
+  S.efree = nf;
+  k_push_free<<<64, 256, 0, st>>>(S.efree, top, old, new_ec);
+  GS_CUDA(cudaGetLastError());
+  k_set_top<<<1, 1, 0, st>>>(S.cnt, new_ec - old);
+  GS_CUDA(cudaGetLastError());
+  e->EC = new_ec;
+  S.EC = new_ec;
+}
+
+void ensure_capacity(gs_engine* e, int64_t extra_units, int64_t extra_edges) {
+  const int64_t need_u = (int64_t)e->next_id + extra_units + 1;
+  if (need_u > e->U) {
+    int64_t nu = std::max<int64_t>(e->U, 1024);
+    while (nu < need_u) nu *= 2;
+    GS_CHECK(nu < (1LL << 30), GS_STATE_ERROR, "unit capacity exceeds 2^30 ids");
+    grow_units(e, (int)nu);
+  }
+  const int64_t need_e = (int64_t)e->n_edges + extra_edges + 1;
+  if (need_e > e->EC) {
+    int64_t ne = std::max<int64_t>(e->EC, 4096);
+    while (ne < need_e) ne *= 2;
+    GS_CHECK(ne < (1LL << 30), GS_STATE_ERROR, "edge capacity exceeds 2^30");
+    grow_edges(e, (int)ne);
+  }
+}
+
+const char* dev_error_name(long long e) {
+  switch (e) {
+    case E_DEGREE: return "unit degree exceeded the device adjacency capacity (64)";
+    case E_UNIT_CAP: return "unit capacity exhausted";
+    case E_EDGE_CAP: return "edge capacity exhausted";
+    case E_STALE: return "stale winner result";
+    case E_UNKNOWN: return "unknown unit";
+    case E_SELF: return "self loop";
+    case E_NOEDGE: return "no such edge";
+    case E_AFF: return "ring-recompute scratch overflow";
+    case E_BADPOS: return "position / threshold must be finite (threshold > 0)";
+    default: return "device error";
+  }
+}
+
+void check_stats(gs_engine* e) {
+  const gs_batch_stats& s = *e->h_stats;
+  e->next_id = (int)s.next_id;
+  e->n_edges = (int)s.edges;
+  e->n_units = (int)s.units;
+  if (s.error) {
+    set_error(std::string("device engine error: ") + dev_error_name(s.error));
+    throw Fail{GS_STATE_ERROR};
+  }
+}
+
+long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
+  ensure_capacity(e, 1, 1);
+  k_op<<<1, 1, 0, e->stream>>>(e->S, e->P, a, e->d_res);
+  GS_CUDA(cudaGetLastError());
+  e->launches++;
+  ++g_launches;
+  GS_CUDA(cudaMemcpyAsync(e->h_res, e->d_res, 3 * sizeof(long long), cudaMemcpyDeviceToHost,
+                          e->stream));
+  Counters hc;
+  GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  e->next_id = hc.next_id;
+  e->n_edges = hc.n_edges;
+  e->n_units = hc.n_units;
+  const long long err = e->h_res[2];
+  if (err == E_UNKNOWN) {
+    set_error("unit is not alive");
+    throw Fail{GS_UNKNOWN_UNIT};
+  }
+  if (err == E_SELF) {
+    set_error("cannot connect a unit to itself");
+    throw Fail{GS_VALUE_ERROR};
+  }
+  if (err == E_NOEDGE) {
+    set_error("no edge between the units");
+    throw Fail{GS_UNKNOWN_UNIT};
+  }
+  if (err > 100) {
+    set_error(std::string("device engine error: ") + dev_error_name(err - 100));
+    throw Fail{err - 100 == E_BADPOS ? GS_VALUE_ERROR : GS_STATE_ERROR};
+  }
+  if (res2) {
+    res2[0] = e->h_res[0];
+    res2[1] = e->h_res[1];
+  }
+  return e->h_res[0];
+}
+
+void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m) {
+  e->batch_no++;
+  k_update_batch<<<1, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m, e->batch_no);
+  GS_CUDA(cudaGetLastError());
+  e->launches++;
+  ++g_launches;
+}
+
+void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinRec* d_rec) {
+  GS_CHECK(e->n_units >= 2, GS_STATE_ERROR, "need at least 2 units to find winners");
+  FindArgs a;
+  a.pos4 = e->S.pos;
+  a.rows = e->S.rows;
+  a.alive = e->S.alive;
+  a.n = e->next_id;  // host upper bound on the row count (grid sizing)
+  a.n_dev = &e->S.cnt->nrows;  // exact row count, read on the device
+  a.sig = d_sig + 3 * lo;
+  a.m = hi - lo;
+  a.out_win = d_rec + lo;
+  a.mode = e->hp.find_mode;
+  const unsigned long long before = g_launches;
+  find_launch(*e->ctx, a, e->stream, e->find_work);
+  e->launches += (long long)(g_launches - before);
+}
+
+}  // namespace
+
+namespace {
+void set_params(gs_engine* e, const gs_params* p) {
+  GS_CHECK(0.0 <= p->eps_n && p->eps_n < p->eps_b && p->eps_b <= 1.0, GS_VALUE_ERROR,
+           "need 0 <= eps_n < eps_b <= 1");
+  GS_CHECK(p->tau_b > 0 && p->tau_b < 1 && p->tau_n > 0 && p->tau_n < 1 && p->h_t > 0 &&
+               p->h_t < 1 && p->rho > 0 && p->rho < 1,
+           GS_VALUE_ERROR, "tau_b, tau_n, h_t, rho must lie in (0, 1)");
+  GS_CHECK(p->max_age >= 0 && p->ring_patience >= 1 && p->stale_factor >= 1, GS_VALUE_ERROR,
+           "bad max_age / ring_patience / stale_factor");
+  GS_CHECK(p->find_mode >= 0 && p->find_mode <= 2, GS_VALUE_ERROR, "bad find mode");
+  e->hp = *p;
+  e->P.eps_b = p->eps_b;
+  e->P.eps_n = p->eps_n;
+  e->P.c_b = 1.0 - p->tau_b;  // engine.py:321
+  e->P.c_n = 1.0 - p->tau_n;  // engine.py:329
+  e->P.h_t = p->h_t;
+  e->P.rho = p->rho;
+  e->P.max_age = p->max_age;
+  e->P.ring_patience = p->ring_patience;
+  e->P.stale_factor = p->stale_factor;
+  e->P.allow_boundary = p->allow_boundary ? 1 : 0;
+}
+}  // namespace
+
+extern "C" gs_status gs_engine_set_params(gs_engine* e, const gs_params* p) {
+  return guarded([&] {
+    GS_CHECK(e && p, GS_VALUE_ERROR, "null argument");
+    set_params(e, p);
+  });
+}
+
+extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t capacity_hint,
+                                      gs_engine** out) {
+  return guarded([&] {
+    GS_CHECK(ctx && p && out, GS_VALUE_ERROR, "null argument");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    gs_engine* e = new gs_engine();
+    e->ctx = ctx;
+    try {
+      set_params(e, p);
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    try {
+      GS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+      GS_CUDA(cudaMalloc(&e->S.cnt, sizeof(Counters)));
+      GS_CUDA(cudaMemsetAsync(e->S.cnt, 0, sizeof(Counters), e->stream));
+      Counters init{};
+      init.next_sweep = kSweepEvery;
+      GS_CUDA(cudaMemcpyAsync(e->S.cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, e->stream));
+      GS_CUDA(cudaStreamSynchronize(e->stream));
+      GS_CUDA(cudaMalloc(&e->S.stats, sizeof(gs_batch_stats)));
+      GS_CUDA(cudaMemset(e->S.stats, 0, sizeof(gs_batch_stats)));
+      GS_CUDA(cudaMalloc(&e->S.aff, sizeof(int32_t) * kAffCap));
+      GS_CUDA(cudaMallocHost(&e->h_stats, sizeof(gs_batch_stats)));
+      memset(e->h_stats, 0, sizeof(gs_batch_stats));
+      GS_CUDA(cudaMalloc(&e->d_res, 4 * sizeof(long long)));
+      GS_CUDA(cudaMallocHost(&e->h_res, 4 * sizeof(long long)));
+      const int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(capacity_hint, 1 << 28));
+      grow_units(e, (int)cap);
+      grow_edges(e, (int)std::min<int64_t>(4 * cap, 1 << 29));
+      GS_CUDA(cudaStreamSynchronize(e->stream));
+    } catch (...) {
+      gs_engine_destroy(e);
+      throw;
+    }
+    *out = e;
+  });
+}
+
+extern "C" void gs_engine_destroy(gs_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->ctx->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  DevState& S = e->S;
+  void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
+                  S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
+                  S.efree, S.iso_list, S.scratch, S.aff, S.cnt, S.stats, e->d_res};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (e->h_stats) cudaFreeHost(e->h_stats);
+  if (e->h_res) cudaFreeHost(e->h_res);
+  if (e->h_sig) cudaFreeHost(e->h_sig);
+  for (auto ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  e->find_work.release();
+  e->sig_buf.release();
+  e->rec_buf.release();
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+extern "C" gs_status gs_engine_add_unit(gs_engine* e, double x, double y, double z,
+                                        double threshold, int64_t* id) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CHECK(std::isfinite(x) && std::isfinite(y) && std::isfinite(z), GS_VALUE_ERROR,
+             "position must be finite");
+    GS_CHECK(std::isfinite(threshold) && threshold > 0.0, GS_VALUE_ERROR,
+             "threshold must be positive and finite");
+    OpArgs a{};
+    a.op = OP_ADD;
+    a.x = x;
+    a.y = y;
+    a.z = z;
+    a.t = threshold;
+    const long long r = run_op(e, a);
+    if (id) *id = r;
+  });
+}
+
+extern "C" gs_status gs_engine_connect_or_reset(gs_engine* e, int64_t a_, int64_t b_,
+                                                int32_t* created) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    OpArgs a{};
+    a.op = OP_CONNECT;
+    a.a = (int)a_;
+    a.b = (int)b_;
+    const long long r = run_op(e, a);
+    if (created) *created = (int32_t)r;
+  });
+}
+
+extern "C" gs_status gs_engine_remove_unit(gs_engine* e, int64_t id) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    OpArgs a{};
+    a.op = OP_REMOVE_UNIT;
+    a.a = (int)id;
+    run_op(e, a);
+  });
+}
+
+extern "C" gs_status gs_engine_remove_edge(gs_engine* e, int64_t a_, int64_t b_) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    OpArgs a{};
+    a.op = OP_REMOVE_EDGE;
+    a.a = (int)a_;
+    a.b = (int)b_;
+    run_op(e, a);
+  });
+}
+
+extern "C" gs_status gs_engine_age_incident_edges(gs_engine* e, int64_t b, int64_t increment,
+                                                  int64_t exclude, int64_t* top) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CHECK(increment >= 0, GS_VALUE_ERROR, "increment must be >= 0");
+    OpArgs a{};
+    a.op = OP_AGE;
+    a.a = (int)b;
+    a.b = (int)exclude;
+    a.i0 = increment;
+    const long long r = run_op(e, a);
+    if (top) *top = r;
+  });
+}
+
+extern "C" gs_status gs_engine_prune(gs_engine* e, int64_t max_age, int64_t* pruned_edges,
+                                     int64_t* units_removed) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CHECK(max_age >= 0, GS_VALUE_ERROR, "max_age must be >= 0");
+    OpArgs a{};
+    a.op = OP_PRUNE;
+    a.i0 = max_age;
+    long long r[2];
+    run_op(e, a, r);
+    if (pruned_edges) *pruned_edges = r[0];
+    if (units_removed) *units_removed = r[1];
+  });
+}
+
+extern "C" gs_status gs_engine_set_unit(gs_engine* e, int64_t id, const double* xyz,
+                                        const double* hab, const double* theta) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    OpArgs a{};
+    a.op = OP_SET;
+    a.a = (int)id;
+    if (xyz) {
+      a.flags |= 1;
+      a.x = xyz[0];
+      a.y = xyz[1];
+      a.z = xyz[2];
+    }
+    if (hab) {
+      a.flags |= 2;
+      a.t = *hab;
+    }
+    if (theta) {
+      a.flags |= 4;
+      a.t2 = *theta;
+    }
+    run_op(e, a);
+  });
+}
+
+extern "C" gs_status gs_engine_step_device(gs_engine* e, const double* d_sig, int64_t m) {
+  return guarded([&] {
+    GS_CHECK(e && d_sig && m > 0, GS_VALUE_ERROR, "bad step arguments");
+    GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
+    ensure_capacity(e, m, 3 * m);
+    WinRec* rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
+    const bool timed = e->timing && !e->ev_pending;
+    if (timed) GS_CUDA(cudaEventRecord(e->ev[0], e->stream));
+    launch_find(e, d_sig, 0, m, rec);
+    if (timed) GS_CUDA(cudaEventRecord(e->ev[1], e->stream));
+    launch_update(e, d_sig, rec, m);
+    if (timed) {
+      GS_CUDA(cudaEventRecord(e->ev[2], e->stream));
+      e->ev_pending = true;
+    }
+    GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
+                            cudaMemcpyDeviceToHost, e->stream));
+  });
+}
+
+namespace {
+void harvest_timing(gs_engine* e) {
+  if (!e->ev_pending) return;
+  float a = 0.f, b = 0.f;
+  GS_CUDA(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
+  GS_CUDA(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
+  e->find_ms += a;
+  e->update_ms += b;
+  e->ev_pending = false;
+}
+}  // namespace
+
+extern "C" gs_status gs_engine_phase_ms(gs_engine* e, int enable, double out[2]) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    if (enable >= 0 && !e->ev[0]) {
+      for (auto& ev : e->ev) GS_CUDA(cudaEventCreate(&ev));
+    }
+    if (enable >= 0) e->timing = enable != 0;
+    if (out) {
+      out[0] = e->find_ms;
+      out[1] = e->update_ms;
+    }
+  });
+}
+
+extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    harvest_timing(e);
+    check_stats(e);
+    if (out) *out = *e->h_stats;
+  });
+}
+
+extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t m,
+                                    gs_batch_stats* out) {
+  return guarded([&] {
+    GS_CHECK(e && signals && m > 0, GS_VALUE_ERROR, "bad step arguments");
+    const size_t bytes = sizeof(double) * 3 * (size_t)m;
+    if (bytes > e->h_sig_cap) {
+      if (e->h_sig) GS_CUDA(cudaFreeHost(e->h_sig));
+      e->h_sig_cap = bytes + bytes / 2;
+      GS_CUDA(cudaMallocHost(&e->h_sig, e->h_sig_cap));
+    }
+    memcpy(e->h_sig, signals, bytes);
+    double* d_sig = (double*)e->sig_buf.get(bytes);
+    GS_CUDA(cudaMemcpyAsync(d_sig, e->h_sig, bytes, cudaMemcpyHostToDevice, e->stream));
+    gs_status st = gs_engine_step_device(e, d_sig, m);
+    if (st != GS_OK) throw Fail{st};
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    harvest_timing(e);
+    check_stats(e);
+    if (out) *out = *e->h_stats;
+  });
+}
+
+extern "C" gs_status gs_engine_find_device(gs_engine* e, const double* d_sig, int64_t lo,
+                                           int64_t hi, void* d_records) {
+  return guarded([&] {
+    GS_CHECK(e && d_sig && d_records && 0 <= lo && lo <= hi, GS_VALUE_ERROR, "bad find range");
+    if (hi == lo) return;
+    launch_find(e, d_sig, lo, hi, (WinRec*)d_records);
+  });
+}
+
+extern "C" gs_status gs_engine_update_device(gs_engine* e, const double* d_sig, int64_t m,
+                                             const void* d_records) {
+  return guarded([&] {
+    GS_CHECK(e && d_sig && d_records && m > 0, GS_VALUE_ERROR, "bad update arguments");
+    ensure_capacity(e, m, 3 * m);
+    launch_update(e, d_sig, (const WinRec*)d_records, m);
+    GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
+                            cudaMemcpyDeviceToHost, e->stream));
+  });
+}
+
+// resolve_and_update with host-given winners (multi.py:99-131): ids + d_winner
+extern "C" gs_status gs_engine_resolve_host(gs_engine* e, const double* signals, int64_t m,
+                                            const int64_t* win_b, const int64_t* win_s,
+                                            const double* d_win, gs_batch_stats* out) {
+  return guarded([&] {
+    GS_CHECK(e && signals && win_b && win_s && d_win && m > 0, GS_VALUE_ERROR,
+             "bad resolve arguments");
+    std::vector<WinRec> recs((size_t)m);
+    for (int64_t j = 0; j < m; ++j) {
+      const bool ok = win_b[j] >= 0 && win_b[j] < (1LL << 31) && win_s[j] >= 0 &&
+                      win_s[j] < (1LL << 31);
+      recs[j].b = ok ? (int32_t)win_b[j] : -1;
+      recs[j].s = ok ? (int32_t)win_s[j] : -1;
+      recs[j].dwin = d_win[j];
+    }
+    const size_t sb = sizeof(double) * 3 * (size_t)m;
+    double* d_sig = (double*)e->sig_buf.get(sb);
+    WinRec* d_rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
+    GS_CUDA(cudaMemcpyAsync(d_sig, signals, sb, cudaMemcpyHostToDevice, e->stream));
+    GS_CUDA(cudaMemcpyAsync(d_rec, recs.data(), sizeof(WinRec) * m, cudaMemcpyHostToDevice,
+                            e->stream));
+    ensure_capacity(e, m, 3 * m);
+    launch_update(e, d_sig, d_rec, m);
+    GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
+                            cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    check_stats(e);
+    if (out) *out = *e->h_stats;
+  });
+}
+
+extern "C" void* gs_engine_stream(gs_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+extern "C" gs_status gs_engine_reserve(gs_engine* e, int64_t n) {
+  return guarded([&] {
+    GS_CHECK(e && n >= 0, GS_VALUE_ERROR, "bad reserve");
+    ensure_capacity(e, n - e->next_id > 0 ? n - e->next_id : 0, 3 * n);
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+extern "C" int64_t gs_engine_launch_count(const gs_engine* e) { return e ? e->launches : 0; }
+
+extern "C" gs_status gs_engine_counts(gs_engine* e, int64_t out[11]) {
+  return guarded([&] {
+    GS_CHECK(e && out, GS_VALUE_ERROR, "null argument");
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    out[0] = hc.n_units;
+    out[1] = hc.n_edges;
+    out[2] = hc.next_id;
+    out[3] = hc.tick;
+    out[4] = hc.next_sweep;
+    out[5] = hc.iso_count;
+    out[6] = hc.ring_counts[0];
+    out[7] = hc.ring_counts[1];
+    out[8] = hc.ring_counts[2];
+    out[9] = hc.untrained;
+    out[10] = hc.nrows;
+  });
+}
+
+namespace {
+template <class T>
+std::vector<T> d2h(const T* p, size_t n, cudaStream_t st) {
+  std::vector<T> v(n);
+  if (n) GS_CUDA(cudaMemcpyAsync(v.data(), p, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+  return v;
+}
+}  // namespace
+
+extern "C" gs_status gs_engine_export_units(gs_engine* e, int64_t cap, int64_t* ids, double* pos,
+                                            double* hab, double* theta, int64_t* ring,
+                                            int64_t* patience, int64_t* last_active,
+                                            int64_t* n_out) {
+  return guarded([&] {
+    GS_CHECK(e && n_out, GS_VALUE_ERROR, "null argument");
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    const size_t n = (size_t)hc.next_id;
+    cudaStream_t st = e->stream;
+    auto alive = d2h(e->S.alive, n, st);
+    auto p4 = d2h(e->S.pos, n, st);
+    auto hb = d2h(e->S.hab, n, st);
+    auto th = d2h(e->S.theta, n, st);
+    auto rg = d2h(e->S.ring, n, st);
+    auto pt = d2h(e->S.patience, n, st);
+    auto la = d2h(e->S.la_val, n, st);
+    GS_CUDA(cudaStreamSynchronize(st));
+    int64_t k = 0;
+    for (size_t u = 0; u < n; ++u) {
+      if (!alive[u]) continue;
+      if (k < cap) {
+        if (ids) ids[k] = (int64_t)u;
+        if (pos) {
+          pos[3 * k] = p4[u].x;
+          pos[3 * k + 1] = p4[u].y;
+          pos[3 * k + 2] = p4[u].z;
+        }
+        if (hab) hab[k] = hb[u];
+        if (theta) theta[k] = th[u];
+        if (ring) ring[k] = rg[u];
+        if (patience) patience[k] = pt[u];
+        if (last_active) last_active[k] = la[u];
+      }
+      ++k;
+    }
+    *n_out = k;
+  });
+}
+
+extern "C" gs_status gs_engine_export_edges(gs_engine* e, int64_t cap, int64_t* abage,
+                                            int64_t* n_out) {
+  return guarded([&] {
+    GS_CHECK(e && n_out, GS_VALUE_ERROR, "null argument");
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    const size_t n = (size_t)hc.next_id;
+    cudaStream_t st = e->stream;
+    auto alive = d2h(e->S.alive, n, st);
+    auto deg = d2h(e->S.deg, n, st);
+    auto adj = d2h(e->S.adj, n * kMaxDeg, st);
+    auto age = d2h(e->S.eage, (size_t)e->EC, st);
+    GS_CUDA(cudaStreamSynchronize(st));
+    std::vector<std::array<int64_t, 3>> out;
+    for (size_t a = 0; a < n; ++a) {
+      if (!alive[a]) continue;
+      for (int k = 0; k < deg[a]; ++k) {
+        const int2 ent = adj[a * kMaxDeg + k];
+        if ((int64_t)a < ent.x) out.push_back({(int64_t)a, (int64_t)ent.x, (int64_t)age[ent.y]});
+      }
+    }
+    std::sort(out.begin(), out.end());
+    const int64_t ne = (int64_t)out.size();
+    for (int64_t i = 0; i < ne && i < cap; ++i) {
+      abage[3 * i] = out[i][0];
+      abage[3 * i + 1] = out[i][1];
+      abage[3 * i + 2] = out[i][2];
+    }
+    *n_out = ne;
+  });
+}
+
+extern "C" gs_status gs_engine_audit(gs_engine* e, int64_t* violations) {
+  return guarded([&] {
+    GS_CHECK(e && violations, GS_VALUE_ERROR, "null argument");
+    unsigned long long* d = (unsigned long long*)e->d_res;
+    GS_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), e->stream));
+    k_audit<<<1, 1024, 0, e->stream>>>(e->S, e->P, d);
+    GS_CUDA(cudaGetLastError());
+    GS_CUDA(cudaMemcpyAsync(e->h_res, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    *violations = (int64_t)e->h_res[0];
+  });
+}

@@ -1,0 +1,266 @@
+// find.cu -- batched best-two ("find winners") kernels for sm_100a.
+//
+// Reference semantics: scan_best_two_into, pkg/src/growsurf/kernels/_scan.pyx:39-98.
+// For every signal j: the rows of the nearest and second-nearest unit and
+// their squared distances, lexicographic on (d2, row), with
+// d2 = ((dx*dx + dy*dy) + dz*dz) in binary64 and dx = p - s.
+//
+// Exact path (GS_FIND_EXACT): every pair in FP64 with the reference rounding
+// sequence.  The m x n pair space is split two ways: CTAs over signal tiles
+// (each thread keeps FS signals in registers) and, when m alone cannot fill
+// the 148 SMs, over contiguous row chunks ("split-n").  Unit rows are staged
+// through shared memory tile by tile and read as broadcasts.  Per-chunk
+// best-two partials are merged in chunk (= row) order with the same strict-<
+// rule, which is exactly the lexicographic (d2, row) top-2 of the union, so
+// the result is independent of the chunking (as it is of the reference's
+// `tile`, test_kernels.py:74-86).
+//
+// Filter path (GS_FIND_FILTER, filter.cu): FP32 top-3 filter and a certified
+// FP64 re-check; bit-identical outputs.
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace gs {
+
+constexpr int kFT = 128;    // threads per CTA
+constexpr int kFS = 4;      // signals per thread
+constexpr int kFTile = 256; // unit rows per shared-memory tile
+
+struct Part {
+  double d1, d2;
+  int32_t i1, i2;
+};
+
+__device__ __forceinline__ bool load_row(const FindArgs& a, int64_t r, double& x, double& y,
+                                         double& z) {
+  if (a.pos4) {
+    const int32_t slot = a.rows ? a.rows[r] : (int32_t)r;
+    if (a.alive && !a.alive[slot]) return false;
+    const double4 p = a.pos4[slot];
+    x = p.x;
+    y = p.y;
+    z = p.z;
+    return true;
+  }
+  x = a.pos[3 * r];
+  y = a.pos[3 * r + 1];
+  z = a.pos[3 * r + 2];
+  return true;
+}
+
+__device__ __forceinline__ void write_result(const FindArgs& a, int64_t j, const Best2& b) {
+  if (a.out_idx) {
+    a.out_idx[2 * j] = b.i1;
+    a.out_idx[2 * j + 1] = b.i2;
+    a.out_d2[2 * j] = b.d1;
+    a.out_d2[2 * j + 1] = b.d2;
+  }
+  if (a.out_win) {
+    WinRec w;
+    w.b = (b.i1 >= 0 && a.rows) ? a.rows[b.i1] : b.i1;
+    w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
+    w.dwin = __dsqrt_rn(b.d1);  // math.sqrt (correctly rounded): multi.py:72-78
+    a.out_win[j] = w;
+  }
+}
+
+__global__ void __launch_bounds__(kFT) find_exact_kernel(FindArgs a, int64_t rows_per_chunk,
+                                                         Part* part) {
+  __shared__ double sx[kFTile], sy[kFTile], sz[kFTile];
+  const int tid = threadIdx.x;
+  const int64_t sig0 = (int64_t)blockIdx.x * (kFT * kFS);
+  const int64_t r_begin = (int64_t)blockIdx.y * rows_per_chunk;
+  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const int64_t r_end = min(n, r_begin + rows_per_chunk);
+
+  double qx[kFS], qy[kFS], qz[kFS];
+  Best2 best[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + tid + k * kFT;
+    best[k].init();
+    if (j < a.m) {
+      qx[k] = a.sig[3 * j];
+      qy[k] = a.sig[3 * j + 1];
+      qz[k] = a.sig[3 * j + 2];
+    } else {
+      qx[k] = qy[k] = qz[k] = 0.0;
+    }
+  }
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += kFTile) {
+    __syncthreads();
+    for (int i = tid; i < kFTile; i += kFT) {
+      const int64_t r = r0 + i;
+      double x = kInf, y = kInf, z = kInf;
+      if (r < r_end && !load_row(a, r, x, y, z)) x = y = z = kInf;
+      sx[i] = x;
+      sy[i] = y;
+      sz[i] = z;
+    }
+    __syncthreads();
+    const int cnt = (int)(r_end - r0 < kFTile ? r_end - r0 : kFTile);
+    for (int i = 0; i < cnt; ++i) {
+      const double px = sx[i], py = sy[i], pz = sz[i];
+      const int32_t row = (int32_t)(r0 + i);
+#pragma unroll
+      for (int k = 0; k < kFS; ++k) best[k].push(dist2_exact(px, py, pz, qx[k], qy[k], qz[k]), row);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + tid + k * kFT;
+    if (j >= a.m) continue;
+    if (part) {
+      Part p;
+      p.d1 = best[k].d1;
+      p.d2 = best[k].d2;
+      p.i1 = best[k].i1;
+      p.i2 = best[k].i2;
+      part[(int64_t)blockIdx.y * a.m + j] = p;
+    } else {
+      write_result(a, j, best[k]);
+    }
+  }
+}
+
+__global__ void find_merge_kernel(FindArgs a, int nchunks, const Part* part) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.m) return;
+  Best2 b;
+  b.init();
+  for (int c = 0; c < nchunks; ++c) {
+    const Part p = part[(int64_t)c * a.m + j];
+    if (p.i1 >= 0) b.push(p.d1, p.i1);
+    if (p.i2 >= 0) b.push(p.d2, p.i2);
+  }
+  write_result(a, j, b);
+}
+
+// forward declaration (filter.cu)
+bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
+
+void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work) {
+  if (a.m <= 0) return;
+  if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
+      find_filter_launch(ctx, a, stream, work))
+    return;
+  const int64_t per_cta = kFT * kFS;
+  const int64_t gx = (a.m + per_cta - 1) / per_cta;
+  const int64_t target = 4LL * ctx.sm_count;
+  int64_t nchunks = std::max<int64_t>(1, (target + gx - 1) / gx);
+  nchunks = std::min<int64_t>(nchunks, std::max<int64_t>(1, (a.n + kFTile - 1) / kFTile));
+  nchunks = std::min<int64_t>(nchunks, 65535);
+  int64_t rows_per_chunk = (a.n + nchunks - 1) / nchunks;
+  if (rows_per_chunk < 1) rows_per_chunk = 1;
+  nchunks = std::max<int64_t>(1, (a.n + rows_per_chunk - 1) / rows_per_chunk);
+  if (a.n == 0) nchunks = 1;
+  Part* part = nullptr;
+  if (nchunks > 1) part = (Part*)work.get(sizeof(Part) * (size_t)nchunks * (size_t)a.m);
+  dim3 grid((unsigned)gx, (unsigned)nchunks);
+  find_exact_kernel<<<grid, kFT, 0, stream>>>(a, rows_per_chunk, part);
+  GS_CUDA(cudaGetLastError());
+  ++g_launches;
+  if (nchunks > 1) {
+    find_merge_kernel<<<(unsigned)((a.m + 255) / 256), 256, 0, stream>>>(a, (int)nchunks, part);
+    GS_CUDA(cudaGetLastError());
+    ++g_launches;
+  }
+}
+
+}  // namespace gs
+
+using namespace gs;
+
+// ---------------------------------------------------------------------------
+// kernel-backend protocol (kernels/__init__.py:6-7): host buffers in and out.
+
+extern "C" gs_status gs_scan_best_two_into(gs_ctx* ctx, const double* pos, int64_t n_rows,
+                                           int64_t n, const double* signals, int64_t m,
+                                           int64_t* out_idx, int64_t out_rows, double* out_d2,
+                                           int64_t out_d2_rows, int64_t tile) {
+  return guarded([&] {
+    GS_CHECK(ctx, GS_VALUE_ERROR, "null context");
+    GS_CHECK(n >= 0 && n <= n_rows, GS_VALUE_ERROR, "n exceeds the position array");
+    GS_CHECK(m >= 0 && out_rows >= m && out_d2_rows >= m, GS_VALUE_ERROR,
+             "output arrays are smaller than the signal batch");
+    GS_CHECK(tile >= 1, GS_VALUE_ERROR, "tile must be >= 1");
+    if (m == 0) return;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    GS_CUDA(cudaSetDevice(ctx->device));
+    const size_t pos_b = sizeof(double) * 3 * (size_t)std::max<int64_t>(n, 1);
+    const size_t sig_b = sizeof(double) * 3 * (size_t)m;
+    const size_t idx_b = sizeof(int64_t) * 2 * (size_t)m;
+    const size_t d2_b = sizeof(double) * 2 * (size_t)m;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    char* d = (char*)ctx->ensure_device(al(pos_b) + al(sig_b) + al(idx_b) + al(d2_b));
+    double* d_pos = (double*)d;
+    double* d_sig = (double*)(d + al(pos_b));
+    int64_t* d_idx = (int64_t*)(d + al(pos_b) + al(sig_b));
+    double* d_d2 = (double*)(d + al(pos_b) + al(sig_b) + al(idx_b));
+    cudaStream_t st = ctx->stream;
+    if (n > 0) GS_CUDA(cudaMemcpyAsync(d_pos, pos, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    GS_CUDA(cudaMemcpyAsync(d_sig, signals, sig_b, cudaMemcpyHostToDevice, st));
+    FindArgs a;
+    a.pos = d_pos;
+    a.n = n;
+    a.sig = d_sig;
+    a.m = m;
+    a.out_idx = d_idx;
+    a.out_d2 = d_d2;
+    a.mode = GS_FIND_AUTO;
+    find_launch(*ctx, a, st, ctx->find_work);
+    GS_CUDA(cudaMemcpyAsync(out_idx, d_idx, idx_b, cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaMemcpyAsync(out_d2, d_d2, d2_b, cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+extern "C" gs_status gs_best_two_single(gs_ctx* ctx, const double* pos, int64_t n_rows, int64_t n,
+                                        double x, double y, double z, int64_t* r1, int64_t* r2,
+                                        double* d2_1, double* d2_2) {
+  const double sig[3] = {x, y, z};
+  int64_t idx[2];
+  double d2[2];
+  gs_status st = gs_scan_best_two_into(ctx, pos, n_rows, n, sig, 1, idx, 1, d2, 1, 1);
+  if (st != GS_OK) return st;
+  *r1 = idx[0];
+  *r2 = idx[1];
+  *d2_1 = d2[0];
+  *d2_2 = d2[1];
+  return GS_OK;
+}
+
+extern "C" gs_status gs_find_device(gs_ctx* ctx, const double* d_pos, int64_t n,
+                                    const double* d_sig, int64_t m, int64_t* d_idx, double* d_d2,
+                                    int mode, void* stream) {
+  return guarded([&] {
+    GS_CHECK(ctx, GS_VALUE_ERROR, "null context");
+    GS_CHECK(n >= 0 && m >= 0, GS_VALUE_ERROR, "negative size");
+    GS_CHECK(mode >= 0 && mode <= 2, GS_VALUE_ERROR, "bad find mode");
+    FindArgs a;
+    a.pos = d_pos;
+    a.n = n;
+    a.sig = d_sig;
+    a.m = m;
+    a.out_idx = d_idx;
+    a.out_d2 = d_d2;
+    a.mode = mode;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    find_launch(*ctx, a, stream ? (cudaStream_t)stream : ctx->stream, ctx->find_work);
+  });
+}
+
+extern "C" gs_status gs_find_last_fallbacks(gs_ctx* ctx, int64_t* count) {
+  return guarded([&] {
+    GS_CHECK(ctx && count, GS_VALUE_ERROR, "null argument");
+    unsigned long long v = 0;
+    if (ctx->d_fallbacks) {
+      GS_CUDA(cudaDeviceSynchronize());
+      GS_CUDA(cudaMemcpy(&v, ctx->d_fallbacks, sizeof(v), cudaMemcpyDeviceToHost));
+    }
+    *count = (int64_t)v;
+  });
+}

@@ -1,0 +1,206 @@
+"""Multi-signal engine on the B200: the reference's training-loop API.
+
+Reference: pkg/src/growsurf/multi.py:44-202 (batch_size, batch_find_winners,
+sequential_executor, resolve_and_update, run_multi) and
+pkg/src/growsurf/parallel.py:107-114 (parallel_executor).
+
+Two drop-in boundaries are offered:
+
+* Executor boundary: ``b200_executor()`` is an ``executor(snapshot, batch)
+  -> list[WinnerResult]`` callable; pass it (or any reference executor) to
+  ``run_multi`` and the find runs where the executor says while the update
+  still runs on the device.
+* Engine boundary (the throughput path): ``run_multi(source, params, seed)``
+  with no executor keeps the whole iteration on the device: per batch one
+  H2D copy of the host-sampled signals, the sm_100a find, the windowed
+  update, the convergence check and one small stats D2H.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+
+import numpy as np
+
+from . import _lib, kernels
+from .metrics import PhaseTimer, RunStats
+from .network import Network, Snapshot
+from .params import BatchOutcome, EngineParams, StateError, WinnerResult, batch_size
+
+__all__ = [
+    "BatchOutcome",
+    "batch_size",
+    "batch_find_winners",
+    "b200_executor",
+    "sequential_executor",
+    "parallel_executor",
+    "resolve_and_update",
+    "run_multi",
+    "RunState",
+]
+
+
+class RunState:
+    """Placeholder for API compatibility: the run state (tick, patience,
+    last_active, sweep clock) lives on the device inside the Network."""
+
+    __slots__ = ()
+
+
+def _scan_batch(snapshot: Snapshot, signals, tile: int | None = None):
+    n = len(snapshot)
+    if n < 2:
+        raise StateError(f"need at least 2 units to find winners, have {n}")
+    signals = np.ascontiguousarray(signals, dtype=np.float64).reshape(-1, 3)
+    m = signals.shape[0]
+    out_idx = np.empty((m, 2), dtype=np.int64)
+    out_d2 = np.empty((m, 2), dtype=np.float64)
+    kernels.scan_best_two_into(np.ascontiguousarray(snapshot.positions, dtype=np.float64), n,
+                               signals, out_idx, out_d2, n if tile is None else tile)
+    return out_idx, out_d2
+
+
+def _to_results(snapshot: Snapshot, out_idx, out_d2) -> list[WinnerResult]:
+    """multi.py:72-78: rows -> ids, d = sqrt(d2) (correctly rounded)."""
+    ids = snapshot.ids
+    sqrt = math.sqrt
+    return [WinnerResult(int(ids[i1]), int(ids[i2]), sqrt(d1), sqrt(d2))
+            for (i1, i2), (d1, d2) in zip(out_idx.tolist(), out_d2.tolist())]
+
+
+def batch_find_winners(snapshot: Snapshot, batch, backend=None,
+                       tile: int | None = None) -> list[WinnerResult]:
+    """Winner pair for every signal, computed on the B200 (multi.py:81-87)."""
+    out_idx, out_d2 = _scan_batch(snapshot, batch, tile)
+    return _to_results(snapshot, out_idx, out_d2)
+
+
+def b200_executor(tile: int | None = None):
+    """Executor running the batched find on the B200."""
+
+    def execute(snapshot: Snapshot, batch) -> list[WinnerResult]:
+        return batch_find_winners(snapshot, batch, tile=tile)
+
+    return execute
+
+
+sequential_executor = b200_executor
+
+
+def parallel_executor(cfg=None, backend=None):
+    """parallel.py:107-114 equivalent: the parallelism is the GPU's."""
+    return b200_executor()
+
+
+def _winner_arrays(winners):
+    m = len(winners)
+    b = np.empty(m, np.int64)
+    s = np.empty(m, np.int64)
+    d = np.empty(m, np.float64)
+    for j, wr in enumerate(winners):
+        b[j] = wr.winner
+        s[j] = wr.second
+        d[j] = wr.d_winner
+    return b, s, d
+
+
+def resolve_and_update(net: Network, params: EngineParams, batch, winners,
+                       state: RunState | None = None, grid=None) -> BatchOutcome:
+    """Winner lock + batch-order update on the device (multi.py:99-131)."""
+    net.set_params(params)
+    batch = np.ascontiguousarray(batch, dtype=np.float64).reshape(-1, 3)
+    b, s, d = _winner_arrays(winners)
+    st = _lib.GsBatchStats()
+    _lib.check(_lib.load_library().gs_engine_resolve_host(net.handle, batch, batch.shape[0], b, s,
+                                                          d, C.byref(st)))
+    net._touch()
+    return BatchOutcome(int(st.processed), int(st.discarded), int(st.inserted))
+
+
+def step(net: Network, batch) -> _lib.GsBatchStats:
+    """One device-resident iteration on a host batch (find + resolve + update)."""
+    batch = np.ascontiguousarray(batch, dtype=np.float64).reshape(-1, 3)
+    st = _lib.GsBatchStats()
+    _lib.check(_lib.load_library().gs_engine_step(net.handle, batch, batch.shape[0],
+                                                  C.byref(st)))
+    net._touch()
+    return st
+
+
+def run_multi(source, params: EngineParams, seed: int, executor=None, *,
+              variant: str = "multi-b200", dataset: str | None = None,
+              find_mode: int = _lib.FIND_AUTO, capacity: int = 4096):
+    """Run the multi-signal engine to convergence or the signal cap.
+
+    Same driver contract as multi.py:134-202: Philox(seed) stream, two seed
+    units from the first two samples, m = batch_size(V) per batch,
+    convergence checked once per batch.  Returns (Network, RunStats).
+    """
+    lib = _lib.load_library()
+    rng = np.random.Generator(np.random.Philox(seed))
+    net = Network(params, capacity=capacity, find_mode=find_mode)
+    net.watch_age_limit(params.max_age)
+    seeds = source.sample(rng, 2)
+    for k in range(2):
+        net.add_unit(seeds[k], params.theta0)
+    timer = PhaseTimer()
+    signals = discarded = iterations = 0
+    converged = False
+    units = 2
+    edges = 0
+    perf = time.perf_counter
+    phase = np.zeros(2, np.float64)
+    if executor is None:
+        _lib.check(lib.gs_engine_phase_ms(net.handle, 1, phase))
+    st = _lib.GsBatchStats()
+    t_start = perf()
+    while signals < params.max_signals:
+        m = batch_size(units, params.batch_cap, params.batch_floor)
+        t0 = perf()
+        batch = np.ascontiguousarray(source.sample(rng, m), dtype=np.float64)
+        t1 = perf()
+        if executor is None:
+            _lib.check(lib.gs_engine_step(net.handle, batch, m, C.byref(st)))
+            t2 = t3 = perf()
+        else:
+            winners = executor(net.snapshot(), batch)
+            t2 = perf()
+            b, s, d = _winner_arrays(winners)
+            _lib.check(lib.gs_engine_resolve_host(net.handle, batch, m, b, s, d, C.byref(st)))
+            net._touch()
+            t3 = perf()
+            timer.find_s += t2 - t1
+            timer.update_s += t3 - t2
+        net._touch()
+        timer.sample_s += t1 - t0
+        signals += m
+        discarded += int(st.discarded)
+        iterations += 1
+        units = int(st.units)
+        edges = int(st.edges)
+        if st.converged:
+            converged = True
+            break
+    total = perf() - t_start
+    if executor is None:
+        _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
+        timer.find_s = phase[0] * 1e-3
+        timer.update_s = phase[1] * 1e-3
+    stats = RunStats(
+        variant=variant,
+        dataset=dataset or getattr(source, "label", "unknown"),
+        seed=seed,
+        iterations=iterations,
+        signals=signals,
+        discarded=discarded,
+        units=units,
+        connections=edges,
+        total_s=total,
+        sample_s=timer.sample_s,
+        find_s=timer.find_s,
+        update_s=timer.update_s,
+        converged=converged,
+    )
+    return net, stats

@@ -72,3 +72,59 @@ def load_golden(name):
 
 def same_numpy(blob) -> bool:
     return str(blob["numpy_version"]) == np.__version__
+
+
+def run_device_trace(name, find_mode=None, executor=None):
+    """Drive the B200 engine batch by batch (the run_multi contract,
+    multi.py:134-185) and record per-batch (m, processed, discarded,
+    inserted) like the golden traces."""
+    import hashlib
+
+    from paper_1503_08294_b200 import FIND_AUTO, Network
+    from paper_1503_08294_b200.multi import resolve_and_update, step
+    from paper_1503_08294_b200.params import EngineParams, batch_size
+
+    case = CASES[name]
+    params = EngineParams(**case["params"])
+    source = make_source(case["source"])
+    rng = np.random.Generator(np.random.Philox(case["seed"]))
+    net = Network(params, find_mode=FIND_AUTO if find_mode is None else find_mode)
+    seeds = source.sample(rng, 2)
+    digest = hashlib.sha256()
+    digest.update(np.ascontiguousarray(seeds).tobytes())
+    for k in range(2):
+        net.add_unit(seeds[k], params.theta0)
+    per_batch = []
+    signals = discarded = iterations = 0
+    units, converged, extra = 2, False, dict(events=0, windows=0, max_degree=0)
+    while signals < params.max_signals:
+        m = batch_size(units, params.batch_cap, params.batch_floor)
+        batch = source.sample(rng, m)
+        digest.update(np.ascontiguousarray(batch).tobytes())
+        if executor is None:
+            st = step(net, batch)
+            out = (int(st.processed), int(st.discarded), int(st.inserted))
+            units = int(st.units)
+            conv = bool(st.converged)
+            extra["events"] += int(st.events)
+            extra["windows"] += int(st.windows)
+            extra["max_degree"] = max(extra["max_degree"], int(st.max_degree))
+        else:
+            winners = executor(net.snapshot(), batch)
+            o = resolve_and_update(net, params, batch, winners)
+            out = (o.processed, o.discarded, o.inserted_units)
+            c = net.counts()
+            units = c["units"]
+            conv = (units >= 4 and c["untrained"] == 0
+                    and c["disk"] + (c["half"] if params.allow_boundary else 0) == units)
+        per_batch.append((m,) + out)
+        signals += m
+        discarded += out[1]
+        iterations += 1
+        if conv:
+            converged = True
+            break
+    c = net.counts()
+    stats = dict(iterations=iterations, signals=signals, discarded=discarded, units=c["units"],
+                 connections=c["edges"], converged=converged, **extra)
+    return net, stats, np.array(per_batch, np.int64).reshape(-1, 4), digest.hexdigest()
