@@ -117,6 +117,9 @@ typedef struct {
   int64_t windows;                        /* parallel windows used by the batch */
   int64_t error;                          /* device error code (0 = none) */
   int64_t max_degree;                     /* largest unit degree seen (capacity check) */
+  int64_t ev_create, ev_insert, ev_prune, ev_sweep; /* serial-path causes (cumulative) */
+  int64_t cyc_serial, cyc_total;          /* update-kernel SM cycles: serial path / all (cumulative) */
+  int64_t cyc_phase[8];                   /* window phases A, scan, B, C1, C2, C3, walk, reset */
 } gs_batch_stats;
 
 typedef struct gs_engine gs_engine;
@@ -177,6 +180,9 @@ gs_status gs_engine_stats(gs_engine *eng, gs_batch_stats *out);
 void *gs_engine_stream(gs_engine *eng);
 /* Pre-size device storage for ids [0, n) (avoids growth inside timed loops). */
 gs_status gs_engine_reserve(gs_engine *eng, int64_t n);
+/* Empty the network in place, keeping device allocations (a fresh
+ * Network() + RunState(), network.py:79-96, engine.py:115-119). */
+gs_status gs_engine_reset(gs_engine *eng);
 /* Device launches issued by the engine so far (kernel count evidence). */
 int64_t gs_engine_launch_count(const gs_engine *eng);
 

@@ -39,7 +39,8 @@ class GsParams(C.Structure):
 class GsBatchStats(C.Structure):
     _fields_ = [(name, C.c_int64) for name in (
         "processed", "discarded", "inserted", "units", "edges", "next_id", "converged",
-        "tick", "events", "windows", "error", "max_degree")]
+        "tick", "events", "windows", "error", "max_degree", "ev_create", "ev_insert",
+        "ev_prune", "ev_sweep", "cyc_serial", "cyc_total")] + [("cyc_phase", C.c_int64 * 8)]
 
 
 _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
@@ -82,6 +83,7 @@ _SIGNATURES = {
     "gs_engine_stream": (_vp, [_vp]),
     "gs_engine_reserve": (C.c_int, [_vp, C.c_int64]),
     "gs_engine_launch_count": (C.c_int64, [_vp]),
+    "gs_engine_reset": (C.c_int, [_vp]),
     "gs_engine_counts": (C.c_int, [_vp, _i64p]),
     "gs_engine_export_units": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          C.POINTER(C.c_int64)]),

@@ -57,6 +57,7 @@ constexpr int kRingDisk = 0, kRingHalf = 1, kRingInc = 2;
 constexpr int kUpdThreads = 1024;
 constexpr long long kSweepEvery = 1024;  // engine.py:98
 constexpr int kAffCap = kMaxDeg * (kMaxDeg + 2) + 64;
+constexpr int kDeferCap = 16384;
 
 enum DevError {
   E_NONE = 0,
@@ -82,6 +83,9 @@ struct Counters {
   int iso_count;
   int error;
   int max_degree;
+  long long ev_create, ev_insert, ev_prune, ev_sweep;
+  long long cyc_serial, cyc_total;
+  long long cyc_phase[8];
   int inserted_start;
   int stale_n;
   int converged;
@@ -114,6 +118,8 @@ struct DevState {
   int32_t* iso_list;    // isolated units (network.py:93 _isolated)
   long long* scratch;   // [2U] sweep (stamp, id) pairs / lonely ids
   int32_t* aff;         // [kAffCap] ring-recompute set
+  int32_t* defer_list;  // [kDeferCap] deferred ring recomputes (event path)
+  int* defer_n;         // non-null: recompute_ring defers (set per launch)
   Counters* cnt;
   gs_batch_stats* stats;
   int U, EC;
@@ -210,6 +216,18 @@ __device__ int classify_ring(const DevState& S, int u) {
 
 // _recompute_ring: network.py:416-422
 __device__ void recompute_ring(const DevState& S, int u) {
+  if (S.defer_n) {
+    // batch-kernel event path: rings are a pure function of the final
+    // adjacency and only read after the topology changes, so collect the
+    // affected units (once each) and reclassify them in parallel afterwards
+    if (S.touchfirst[u] != -2) {
+      S.touchfirst[u] = -2;
+      const int k = (*S.defer_n)++;
+      if (k < kDeferCap) S.defer_list[k] = u;
+      else set_err(S, E_AFF);
+    }
+    return;
+  }
   const int nw = classify_ring(S, u);
   const int old = S.ring[u];
   if (nw != old) {
@@ -524,7 +542,9 @@ __device__ int serial_update_part1(const DevState& S, const Params& P, int b, in
   const long long tick = ++c->tick;
   touch_active(S, b, tick, 0);
   touch_active(S, s, tick, 1);
-  if (connect_or_reset(S, b, s) < 0) return 0;
+  const int created = connect_or_reset(S, b, s);
+  if (created < 0) return 0;
+  if (created) c->ev_create++;
   int32_t over[kMaxDeg];
   int nover = 0;
   age_incident(S, P, b, s, 1, over, &nover);
@@ -555,9 +575,11 @@ __device__ int serial_update_part1(const DevState& S, const Params& P, int b, in
     connect_or_reset(S, r, s);
     if (find_slot(S, b, s) >= 0) remove_edge(S, b, s);
     touch_active(S, r, tick, 2);
+    c->ev_insert++;
   }
   int pe, pu;
   prune_winner(S, P, b, over, nover, &pe, &pu);
+  if (pe || pu) c->ev_prune++;
   return tick >= c->next_sweep ? 1 : 0;
 }
 
@@ -566,7 +588,11 @@ __device__ void serial_update_part2(const DevState& S, const Params& P, int b, i
                                     bool sweep_fired) {
   Counters* c = S.cnt;
   if (sweep_fired) {
-    if (swept_n > 0) sweep_apply(S, P, S.scratch, swept_n);
+    if (swept_n > 0) {
+      const int before = c->n_units;
+      sweep_apply(S, P, S.scratch, swept_n);
+      if (c->n_units != before) c->ev_sweep++;
+    }
     c->next_sweep = c->tick + kSweepEvery;
   }
   if (S.alive[b]) adapt_threshold(S, P, b);
@@ -642,288 +668,7 @@ __device__ int block_sum(int v, int* s_warp) {
   return total;
 }
 
-// ---------------------------------------------------------------------------
-// window helpers
-
-// replay unit u's updates from this window's committed signals in batch
-// order (the exact per-unit rounding sequence of the sequential loop)
-__device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
-                          int jstar) {
-  const int2* A = S.adj + (size_t)u * kMaxDeg;
-  const int d = S.deg[u];
-  const int jself = S.firstwin[u];
-  double4 p = S.pos[u];
-  const double h0 = S.hab[u];
-  double h = h0;
-  int cur = -1;
-  while (true) {
-    int nxt = 0x7fffffff;
-    bool self = false;
-    if (jself < jstar && jself > cur) {
-      nxt = jself;
-      self = true;
-    }
-    for (int k = 0; k < d; ++k) {
-      const int jw = S.firstwin[A[k].x];
-      if (jw < jstar && jw > cur && jw < nxt) {
-        nxt = jw;
-        self = false;
-      }
-    }
-    if (nxt == 0x7fffffff) break;
-    cur = nxt;
-    const double x = sig[3 * (size_t)nxt], y = sig[3 * (size_t)nxt + 1], z = sig[3 * (size_t)nxt + 2];
-    if (self) {
-      move_toward(p, P.eps_b, x, y, z);
-      h = dmul(h, P.c_b);
-    } else {
-      move_toward(p, P.eps_n, x, y, z);
-      h = dmul(h, P.c_n);
-    }
-  }
-  S.pos[u] = p;
-  S.hab[u] = h;
-  if (h0 >= P.h_t && h < P.h_t) atomicSub(&S.cnt->untrained, 1);
-}
-
-__device__ __forceinline__ double pow_chain(double h, double c, int k) {
-  for (int i = 0; i < k; ++i) h = dmul(h, c);
-  return h;
-}
-
-// ---------------------------------------------------------------------------
-// the batch update kernel: one CTA of 1024 threads
-
-__global__ void __launch_bounds__(kUpdThreads, 1)
-    k_update_batch(DevState S, Params P, const double* __restrict__ sig,
-                   const WinRec* __restrict__ rec, int m, int batch_no) {
-  __shared__ int s_warp[33];
-  __shared__ int s_i[4];
-  __shared__ long long s_ll[2];
-  Counters* c = S.cnt;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    c->processed = c->discarded = c->events = c->windows = 0;
-    c->inserted_start = c->next_id;
-    c->stale_n = 0;
-  }
-  __syncthreads();
-  int j0 = 0;
-  while (j0 < m) {
-    const int j = j0 + tid;
-    const bool act = j < m;
-    const int next_id = c->next_id;
-    int b = -1, s = -1;
-    double dw = 0.0;
-    bool cand = false;
-    if (act) {
-      const WinRec r = rec[j];
-      b = r.b;
-      s = r.s;
-      dw = r.dwin;
-      cand = b >= 0 && s >= 0 && b < next_id && s < next_id && b != s && S.alive[b] &&
-             S.alive[s] && S.claim[b] != batch_no;
-    }
-    if (cand) atomicMin(&S.firstwin[b], j);
-    __syncthreads();
-    const bool proc = cand && S.firstwin[b] == j;
-    int nproc;
-    const int rank = block_excl_scan(proc ? 1 : 0, s_warp, &nproc);
-    const long long tick_j = c->tick + rank + 1;
-    bool ev = false;
-    int newpat = -2;
-    bool shrink = false;
-    bool absent_b = false, absent_s = false;
-    if (proc) {
-      ev = c->iso_count > 0 || tick_j >= c->next_sweep;
-      const int db = S.deg[b];
-      const int2* B = S.adj + (size_t)b * kMaxDeg;
-      bool found = false;
-      int kcn = 0;
-      for (int k = 0; k < db; ++k) {
-        const int2 ent = B[k];
-        const int v = ent.x;
-        const int jv = S.firstwin[v];
-        if (v == s) found = true;
-        if (jv < j) kcn++;
-        if (v != s) {
-          int age = S.eage[ent.y];
-          if (jv < j) age = (rec[jv].s == b) ? 0 : age + 1;
-          if (age + 1 > P.max_age) ev = true;
-        }
-      }
-      if (!found) ev = true;  // connect_or_reset would create b-s
-      const double hb = dmul(pow_chain(S.hab[b], P.c_n, kcn), P.c_b);
-      if (dw > S.theta[b] && hb < P.h_t) ev = true;  // insertion
-      if (!ev) {
-        // adapt_threshold at time j (engine.py:208-265)
-        const int ring = S.ring[b];
-        if (ring == kRingDisk || (P.allow_boundary && ring == kRingHalf)) {
-          newpat = 0;
-        } else if (hb < P.h_t) {
-          bool ok = true;
-          for (int k = 0; k < db && ok; ++k) {
-            const int v = B[k].x;
-            const int jv = S.firstwin[v];
-            const bool vwon = jv < j;
-            const int dv = S.deg[v];
-            const int2* V = S.adj + (size_t)v * kMaxDeg;
-            int k1 = 0, k2 = 0;
-            for (int q = 0; q < dv; ++q) {
-              const int jw = S.firstwin[V[q].x];
-              if (jw <= j) {
-                if (vwon && jw > jv) k2++;
-                else k1++;
-              }
-            }
-            double hv = pow_chain(S.hab[v], P.c_n, k1);
-            if (vwon) hv = dmul(hv, P.c_b);
-            hv = pow_chain(hv, P.c_n, k2);
-            if (hv >= P.h_t) ok = false;
-          }
-          if (ok) {
-            int cnt = S.patience[b] + 1;
-            if (cnt >= P.ring_patience) {
-              shrink = true;
-              cnt = 0;
-            }
-            newpat = cnt;
-          }
-        }
-      }
-      absent_b = S.la_val[b] == -1;
-      absent_s = S.la_val[s] == -1;
-    }
-    const int wend = min(j0 + kUpdThreads, m);
-    int jstar = block_min((proc && ev) ? j : 0x7fffffff, s_warp);
-    if (jstar == 0x7fffffff) jstar = wend;
-    const bool com = proc && j < jstar;
-    if (com) {
-      S.claim[b] = batch_no;
-      if (absent_b) atomicMin(&S.la_stamp[b], 3 * tick_j);
-      atomicMax(&S.la_val[b], tick_j);
-      if (absent_s) atomicMin(&S.la_stamp[s], 3 * tick_j + 1);
-      atomicMax(&S.la_val[s], tick_j);
-      atomicMin(&S.touchfirst[b], j);
-      const int db = S.deg[b];
-      const int2* B = S.adj + (size_t)b * kMaxDeg;
-      for (int k = 0; k < db; ++k) atomicMin(&S.touchfirst[B[k].x], j);
-      if (newpat != -2) {
-        S.patience[b] = newpat;
-        if (shrink) S.theta[b] = dmul(S.theta[b], P.rho);
-      }
-    }
-    __syncthreads();
-    if (com) {
-      if (S.touchfirst[b] == j) walk_unit(S, P, sig, b, jstar);
-      const int db = S.deg[b];
-      const int2* B = S.adj + (size_t)b * kMaxDeg;
-      for (int k = 0; k < db; ++k) {
-        const int2 ent = B[k];
-        const int v = ent.x;
-        if (S.touchfirst[v] == j) walk_unit(S, P, sig, v, jstar);
-        const int jv = S.firstwin[v];
-        if (jv < jstar && jv > j) continue;  // v's signal replays this edge
-        int age = S.eage[ent.y];
-        if (jv < j) age = (rec[jv].s == b) ? 0 : age + 1;
-        age = (v == s) ? 0 : age + 1;
-        S.eage[ent.y] = age;
-      }
-    }
-    const int ncom = block_sum(com ? 1 : 0, s_warp);
-    const int ndisc = block_sum((act && j < jstar && !proc) ? 1 : 0, s_warp);
-    if (tid == 0) {
-      c->tick += ncom;
-      c->processed += ncom;
-      c->discarded += ndisc;
-      c->windows++;
-    }
-    __syncthreads();
-    if (cand) S.firstwin[b] = kNone32;
-    if (com) {
-      S.touchfirst[b] = kNone32;
-      const int db = S.deg[b];
-      const int2* B = S.adj + (size_t)b * kMaxDeg;
-      for (int k = 0; k < db; ++k) S.touchfirst[B[k].x] = kNone32;
-    }
-    __syncthreads();
-    if (jstar < wend) {
-      // the event signal, executed exactly as update_single
-      if (tid == 0) {
-        const WinRec r = rec[jstar];
-        S.claim[r.b] = batch_no;
-        const int fired = serial_update_part1(S, P, r.b, r.s, r.dwin, sig[3 * (size_t)jstar],
-                                              sig[3 * (size_t)jstar + 1],
-                                              sig[3 * (size_t)jstar + 2]);
-        c->processed++;
-        c->events++;
-        c->stale_n = 0;
-        s_i[0] = fired;
-        s_ll[0] = fired ? sweep_cutoff(S, P) : 0;
-        s_i[1] = r.b;
-      }
-      __syncthreads();
-      const int fired = s_i[0];
-      const long long cutoff = s_ll[0];
-      if (fired && cutoff > 0) {
-        const int nid = c->next_id;
-        for (int u = tid; u < nid; u += kUpdThreads) {
-          const long long t = S.la_val[u];
-          if (t != -1 && t < cutoff) {
-            const int q = atomicAdd(&c->stale_n, 1);
-            S.scratch[2 * q] = S.la_stamp[u];
-            S.scratch[2 * q + 1] = u;
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0) serial_update_part2(S, P, s_i[1], c->stale_n, fired != 0);
-      __syncthreads();
-      j0 = jstar + 1;
-    } else {
-      j0 = wend;
-    }
-    __syncthreads();
-  }
-  // compact rows when dead entries exceed 1/8 (keeps id order)
-  if (c->ndead_rows * 8 > c->nrows) {
-    const int n = c->nrows;
-    int out = 0;
-    for (int base = 0; base < n; base += kUpdThreads) {
-      const int r = base + tid;
-      const int id = r < n ? S.rows[r] : -1;
-      const int keep = (id >= 0 && S.alive[id]) ? 1 : 0;
-      int tot;
-      const int rk = block_excl_scan(keep, s_warp, &tot);
-      if (keep) S.rows[out + rk] = id;
-      out += tot;
-      __syncthreads();
-    }
-    if (tid == 0) {
-      c->nrows = out;
-      c->ndead_rows = 0;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // is_converged: engine.py:358-365 (max(h) < h_t <=> no untrained unit)
-    int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
-    c->converged = (c->n_units >= 4 && ok == c->n_units && c->untrained == 0) ? 1 : 0;
-    gs_batch_stats* st = S.stats;
-    st->processed = c->processed;
-    st->discarded = c->discarded;
-    st->inserted = c->next_id - c->inserted_start;
-    st->units = c->n_units;
-    st->edges = c->n_edges;
-    st->next_id = c->next_id;
-    st->converged = c->converged;
-    st->tick = c->tick;
-    st->events = c->events;
-    st->windows = c->windows;
-    st->error = c->error;
-    st->max_degree = c->max_degree;
-  }
-}
+#include "update_kernel.cuh"
 
 // ---------------------------------------------------------------------------
 // Network API operations (single thread; not on the hot path)
@@ -1359,6 +1104,7 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
       GS_CUDA(cudaMalloc(&e->S.stats, sizeof(gs_batch_stats)));
       GS_CUDA(cudaMemset(e->S.stats, 0, sizeof(gs_batch_stats)));
       GS_CUDA(cudaMalloc(&e->S.aff, sizeof(int32_t) * kAffCap));
+      GS_CUDA(cudaMalloc(&e->S.defer_list, sizeof(int32_t) * kDeferCap));
       GS_CUDA(cudaMallocHost(&e->h_stats, sizeof(gs_batch_stats)));
       memset(e->h_stats, 0, sizeof(gs_batch_stats));
       GS_CUDA(cudaMalloc(&e->d_res, 4 * sizeof(long long)));
@@ -1382,7 +1128,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   DevState& S = e->S;
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
-                  S.efree, S.iso_list, S.scratch, S.aff, S.cnt, S.stats, e->d_res};
+                  S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (e->h_stats) cudaFreeHost(e->h_stats);
@@ -1641,6 +1387,36 @@ extern "C" gs_status gs_engine_reserve(gs_engine* e, int64_t n) {
     GS_CHECK(e && n >= 0, GS_VALUE_ERROR, "bad reserve");
     ensure_capacity(e, n - e->next_id > 0 ? n - e->next_id : 0, 3 * n);
     GS_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
+// Empty the network in place (no reallocation): a fresh Network() + RunState().
+extern "C" gs_status gs_engine_reset(gs_engine* e) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    cudaStream_t st = e->stream;
+    DevState& S = e->S;
+    const int64_t U = e->U;
+    GS_CUDA(cudaMemsetAsync(S.alive, 0, U, st));
+    GS_CUDA(cudaMemsetAsync(S.deg, 0, sizeof(int32_t) * U, st));
+    fill_i32(S.firstwin, U, kNone32, st);
+    fill_i32(S.touchfirst, U, kNone32, st);
+    fill_i32(S.claim, U, -1, st);
+    fill_i32(S.iso_pos, U, -1, st);
+    fill_i64(S.la_val, U, -1, st);
+    fill_i64(S.la_stamp, U, kNone64, st);
+    k_push_free<<<64, 256, 0, st>>>(S.efree, 0, 0, e->EC);
+    GS_CUDA(cudaGetLastError());
+    Counters init{};
+    init.next_sweep = kSweepEvery;
+    init.efree_top = e->EC;
+    GS_CUDA(cudaMemcpyAsync(S.cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
+    GS_CUDA(cudaMemsetAsync(S.stats, 0, sizeof(gs_batch_stats), st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    e->next_id = e->n_edges = e->n_units = 0;
+    memset(e->h_stats, 0, sizeof(gs_batch_stats));
+    e->find_ms = e->update_ms = 0.0;
+    e->ev_pending = false;
   });
 }
 

@@ -25,7 +25,7 @@
 namespace gs {
 
 constexpr int kFT = 128;    // threads per CTA
-constexpr int kFS = 4;      // signals per thread
+constexpr int kMinChunk = 64; // fewest unit rows per split-n chunk
 constexpr int kFTile = 256; // unit rows per shared-memory tile
 
 struct Part {
@@ -66,6 +66,7 @@ __device__ __forceinline__ void write_result(const FindArgs& a, int64_t j, const
   }
 }
 
+template <int kFS>  // signals per thread
 __global__ void __launch_bounds__(kFT) find_exact_kernel(FindArgs a, int64_t rows_per_chunk,
                                                          Part* part) {
   __shared__ double sx[kFTile], sy[kFTile], sz[kFTile];
@@ -147,11 +148,13 @@ void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work)
   if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
       find_filter_launch(ctx, a, stream, work))
     return;
-  const int64_t per_cta = kFT * kFS;
+  // few signals -> one per thread and more row chunks; many -> 4 per thread
+  const int fs = a.m >= 4LL * ctx.sm_count * kFT * 4 ? 4 : 1;
+  const int64_t per_cta = (int64_t)kFT * fs;
   const int64_t gx = (a.m + per_cta - 1) / per_cta;
   const int64_t target = 4LL * ctx.sm_count;
   int64_t nchunks = std::max<int64_t>(1, (target + gx - 1) / gx);
-  nchunks = std::min<int64_t>(nchunks, std::max<int64_t>(1, (a.n + kFTile - 1) / kFTile));
+  nchunks = std::min<int64_t>(nchunks, std::max<int64_t>(1, (a.n + kMinChunk - 1) / kMinChunk));
   nchunks = std::min<int64_t>(nchunks, 65535);
   int64_t rows_per_chunk = (a.n + nchunks - 1) / nchunks;
   if (rows_per_chunk < 1) rows_per_chunk = 1;
@@ -160,7 +163,10 @@ void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work)
   Part* part = nullptr;
   if (nchunks > 1) part = (Part*)work.get(sizeof(Part) * (size_t)nchunks * (size_t)a.m);
   dim3 grid((unsigned)gx, (unsigned)nchunks);
-  find_exact_kernel<<<grid, kFT, 0, stream>>>(a, rows_per_chunk, part);
+  if (fs == 4)
+    find_exact_kernel<4><<<grid, kFT, 0, stream>>>(a, rows_per_chunk, part);
+  else
+    find_exact_kernel<1><<<grid, kFT, 0, stream>>>(a, rows_per_chunk, part);
   GS_CUDA(cudaGetLastError());
   ++g_launches;
   if (nchunks > 1) {

@@ -85,6 +85,21 @@ class Network:
     def handle(self):
         return self._h
 
+    def stream_handle(self) -> int:
+        """The engine's cudaStream_t as an integer (for torch.cuda.ExternalStream)."""
+        return int(self._lib.gs_engine_stream(self._h) or 0)
+
+    def reset(self) -> None:
+        """Empty the network in place (a fresh Network + RunState), keeping allocations."""
+        _lib.check(self._lib.gs_engine_reset(self._h))
+        self._touch()
+
+    def reserve(self, n_ids: int) -> None:
+        _lib.check(self._lib.gs_engine_reserve(self._h, int(n_ids)))
+
+    def launch_count(self) -> int:
+        return int(self._lib.gs_engine_launch_count(self._h))
+
     def set_params(self, params: EngineParams) -> None:
         if params is self._params:
             return

@@ -180,50 +180,62 @@ class CloudSource:
 
 
 class DoubleTorusSource:
-    """Genus-2 surface: a tube around a lemniscate of Bernoulli.
+    """Genus-2 surface: smooth union of two overlapping tori (an "eight").
 
-    Implicit surface F(x, y, z) = g(x, y)^2 + z^2 - r^2 = 0 with
-    g = (x^2 + y^2)^2 - a^2 (x^2 - y^2).  The figure-eight centre curve has
-    one crossing, so its thickened tube bounds two holes (genus 2); F is
-    smooth for r > 0.  Points are drawn uniformly in the bounding box, kept
-    near the surface, and Newton-projected onto F = 0.  Not area-uniform;
-    used only to materialise deterministic benchmark clouds.
+    Signed distance to torus i: T_i = |(rho_i - R, z)| - r with
+    rho_i = |(x -/+ c, y)|; blended union F = T1 + T2 - sqrt(T1^2 + T2^2 + d^2)
+    (an R-function union whose crease along the intersection is rounded over
+    a width ~d).  The tori overlap (c < R + r), so the union's boundary is one
+    closed surface with two handles.  Points are drawn uniformly in the
+    bounding box, kept near F = 0 and Newton-projected onto it.  Not exactly
+    area-uniform; used only to materialise deterministic benchmark clouds
+    that both the reference and this package read through CloudSource.
     """
 
-    def __init__(self, a: float = 1.0, r: float = 0.12):
-        if not (a > 0.0 and r > 0.0):
-            raise ValueError("need a > 0 and r > 0")
-        self.a = float(a)
-        self.r = float(r)
-        self.label = f"double-torus:{a:g},{r:g}"
+    def __init__(self, major: float = 1.0, minor: float = 0.4, offset: float = 1.1,
+                 blend: float = 0.1):
+        if not (major > minor > 0.0 and 0.0 < offset < major + minor and blend > 0.0):
+            raise ValueError("need major > minor > 0, 0 < offset < major + minor, blend > 0")
+        self.major, self.minor, self.offset, self.blend = map(float, (major, minor, offset, blend))
+        self.label = f"double-torus:{major:g},{minor:g},{offset:g}"
 
     def _field(self, p):
         x, y, z = p[:, 0], p[:, 1], p[:, 2]
-        a2 = self.a * self.a
-        q = x * x + y * y
-        g = q * q - a2 * (x * x - y * y)
-        gx = 4.0 * q * x - 2.0 * a2 * x
-        gy = 4.0 * q * y + 2.0 * a2 * y
-        f = g * g + z * z - self.r * self.r
-        grad = np.stack([2.0 * g * gx, 2.0 * g * gy, 2.0 * z], axis=1)
+        vals, grads = [], []
+        for sgn in (-1.0, 1.0):
+            dx = x + sgn * self.offset
+            rho = np.sqrt(dx * dx + y * y)
+            rho = np.maximum(rho, 1e-12)
+            q = rho - self.major
+            dist = np.sqrt(q * q + z * z)
+            dist = np.maximum(dist, 1e-12)
+            vals.append(dist - self.minor)
+            grads.append(np.stack([q / dist * dx / rho, q / dist * y / rho, z / dist], axis=1))
+        t1, t2 = vals
+        root = np.sqrt(t1 * t1 + t2 * t2 + self.blend * self.blend)
+        f = t1 + t2 - root
+        grad = grads[0] * (1.0 - t1 / root)[:, None] + grads[1] * (1.0 - t2 / root)[:, None]
         return f, grad
 
     def sample(self, rng: np.random.Generator, n: int) -> np.ndarray:
         lo, hi = self.bounds()
-        out = np.empty((0, 3))
-        while out.shape[0] < n:
-            p = lo + (hi - lo) * rng.random((4 * n, 3))
+        chunks, have = [], 0
+        while have < n:
+            p = lo + (hi - lo) * rng.random((2 * n + 1024, 3))
             f, _ = self._field(p)
-            p = p[np.abs(f) < 0.5 * self.r * self.r]
-            for _ in range(30):
+            p = p[np.abs(f) < 0.25 * self.minor]
+            for _ in range(12):
                 f, grad = self._field(p)
-                gg = np.sum(grad * grad, axis=1)
-                p = p - (f / np.maximum(gg, 1e-300))[:, None] * grad
+                gg = np.maximum(np.sum(grad * grad, axis=1), 1e-300)
+                p = p - (f / gg)[:, None] * grad
             f, _ = self._field(p)
-            out = np.concatenate([out, p[np.abs(f) < 1e-12]])
-        return out[:n]
+            p = p[np.abs(f) < 1e-9]
+            chunks.append(p)
+            have += p.shape[0]
+        return np.concatenate(chunks)[:n]
 
     def bounds(self):
-        a = self.a
-        reach = a * 1.2 + self.r
-        return np.array([-reach, -0.5 * a, -1.2 * self.r]), np.array([reach, 0.5 * a, 1.2 * self.r])
+        reach = self.offset + self.major + self.minor + self.blend
+        side = self.major + self.minor + self.blend
+        h = self.minor + self.blend
+        return np.array([-reach, -side, -h]), np.array([reach, side, h])

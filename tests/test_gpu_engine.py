@@ -224,3 +224,29 @@ class TestNetworkApi:
         net.remove_unit(3)
         assert net.edge_count == 3 and not net.all_rings_surface()
         net.audit()
+
+
+@pytest.mark.slow
+def test_cfg3_headline_run_matches_reference():
+    """BASELINE config 3 (1M-point genus-2 cloud, m=4096, theta0=0.1): the
+    device run to convergence equals the reference's own full run
+    (tests/golden/make_cfg3_golden.py, 430 s on 8 cores) bit for bit."""
+    import os
+
+    from paper_1503_08294_b200 import extract_mesh, genus, manifold_check, run_multi, workloads
+
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "run_cfg3_final.npz"))
+    if str(gold["numpy_version"]) != np.__version__:
+        pytest.skip("golden made with another numpy")
+    src, params, seed, _ = workloads.make("cfg3")
+    net, st = run_multi(src, params, seed, capacity=8192)
+    assert (st.signals, st.discarded, st.iterations, st.units, st.connections, st.converged) == (
+        int(gold["stat_signals"]), int(gold["stat_discarded"]), int(gold["stat_iterations"]),
+        int(gold["stat_units"]), int(gold["stat_connections"]), bool(gold["stat_converged"]))
+    got = net.export()
+    assert np.array_equal(got["ids"], gold["ids"])
+    assert np.array_equal(got["edges"], gold["edges"])
+    for k in ("pos", "hab", "theta"):
+        assert np.array_equal(got[k].view(np.int64), gold[k].view(np.int64)), k
+    mesh = extract_mesh(net)
+    assert manifold_check(mesh) == "closed" and genus(mesh) == 2
