@@ -46,7 +46,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gs {
 
@@ -89,6 +93,8 @@ struct Counters {
   int inserted_start;
   int stale_n;
   int converged;
+  int nwalk, defer_n, ev_fired, ev_b;
+  long long ev_cutoff;
 };
 
 struct Params {
@@ -1024,7 +1030,7 @@ long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
 
 void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m) {
   e->batch_no++;
-  k_update_batch<<<1, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m, e->batch_no);
+  k_update_batch<<<kCluster, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m, e->batch_no);
   GS_CUDA(cudaGetLastError());
   e->launches++;
   ++g_launches;

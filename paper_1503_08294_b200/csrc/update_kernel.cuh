@@ -2,8 +2,8 @@
 //
 // Windowed segmented replay of the reference's sequential update loop
 // (multi.py:120-130 -> engine.py:283-355); see the engine.cu header for the
-// argument.  One CTA of 1024 threads processes windows of up to kWin
-// signals:
+// argument.  One cluster of 8 CTAs x 1024 threads (8 SMs, cluster barriers
+// between phases) processes windows of up to 8192 signals:
 //
 //   A  candidates: alive winner and second, winner not yet claimed this
 //      batch; atomicMin(firstwin[b], j) -- the first candidate per winner is
@@ -24,8 +24,6 @@
 //   D  the event signal runs exactly as update_single on thread 0 (the
 //      sweep's stale scan is block-parallel); the next window starts after it.
 
-constexpr int kSigPerThread = 4;
-constexpr int kWin = kUpdThreads * kSigPerThread;
 
 // replay unit u's updates from the committed signals (< jstar) of this window
 __device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
@@ -183,85 +181,163 @@ __device__ int event_part1b(const DevState& S, const Params& P, int b, int s, do
   return tick >= c->next_sweep ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kUpdThreads, 1)
+// ---------------------------------------------------------------------------
+// cluster primitives: kCluster CTAs x 1024 threads cooperate on one window;
+// cross-CTA values travel through distributed shared memory and every
+// exchange is fenced by the hardware cluster barrier.
+
+constexpr int kCluster = 8;
+constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
+constexpr int kWalkCap = 6 * kUpdThreads;      // per-CTA replay queue (overflow: global)
+
+__device__ __forceinline__ void push_walk(const DevState& S, int* s_walk, int* s_nwalk, int u) {
+  const int k = atomicAdd(s_nwalk, 1);
+  if (k < kWalkCap) s_walk[k] = u;
+  else S.scratch[atomicAdd(&S.cnt->nwalk, 1)] = u;
+}
+
+// exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
+// used with alternating parity so a CTA running one call ahead cannot
+// overwrite values another CTA has not read yet.
+__device__ int cl_excl_scan(int v, int* s_warp, int (*s_cta)[kCluster], int& parity, int* total) {
+  cg::cluster_group cl = cg::this_cluster();
+  int btot;
+  const int r = block_excl_scan(v, s_warp, &btot);
+  const int me = (int)cl.block_rank();
+  if (threadIdx.x < kCluster) {
+    int* dst = cl.map_shared_rank(&s_cta[parity][0], threadIdx.x);
+    dst[me] = btot;
+  }
+  cl.sync();
+  int off = 0, tot = 0;
+#pragma unroll
+  for (int q = 0; q < kCluster; ++q) {
+    const int t = s_cta[parity][q];
+    off += q < me ? t : 0;
+    tot += t;
+  }
+  parity ^= 1;
+  *total = tot;
+  return off + r;
+}
+
+__device__ int cl_min(int v, int* s_warp, int (*s_cta)[kCluster], int& parity) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int bmin = block_min(v, s_warp);
+  const int me = (int)cl.block_rank();
+  if (threadIdx.x < kCluster) {
+    int* dst = cl.map_shared_rank(&s_cta[parity][0], threadIdx.x);
+    dst[me] = bmin;
+  }
+  cl.sync();
+  int x = 0x7fffffff;
+#pragma unroll
+  for (int q = 0; q < kCluster; ++q) x = min(x, s_cta[parity][q]);
+  parity ^= 1;
+  return x;
+}
+
+__device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_ctal)[kCluster],
+                               int& parity) {
+  cg::cluster_group cl = cg::this_cluster();
+  const long long bmin = block_min_ll(v, s_ll32);
+  const int me = (int)cl.block_rank();
+  if (threadIdx.x < kCluster) {
+    long long* dst = cl.map_shared_rank(&s_ctal[parity][0], threadIdx.x);
+    dst[me] = bmin;
+  }
+  cl.sync();
+  long long x = 0x7fffffffffffffffLL;
+#pragma unroll
+  for (int q = 0; q < kCluster; ++q) x = s_ctal[parity][q] < x ? s_ctal[parity][q] : x;
+  parity ^= 1;
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// the batch update kernel: one cluster of kCluster CTAs (8 SMs)
+
+__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 1)
     k_update_batch(DevState S, Params P, const double* __restrict__ sig,
                    const WinRec* __restrict__ rec, int m, int batch_no) {
+  cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_warp[33];
   __shared__ long long s_ll32[33];
-  __shared__ int s_plist[kWin];  // processed signals of the window, batch order
-  __shared__ int s_pat[kWin];    // adapt_threshold outcome: -2 none, else patience | shrink<<30
+  __shared__ int s_cta[2][kCluster];
+  __shared__ long long s_ctal[2][kCluster];
+  __shared__ int s_plist[kUpdThreads];  // this CTA's slice of the window's processed list
+  __shared__ int s_pat[kUpdThreads];    // adapt_threshold outcome: -2 none, else patience | shrink<<30
+  __shared__ unsigned char s_abs[kUpdThreads];  // last_active absent at window start: b | s<<1
+  __shared__ int s_walk[kWalkCap];  // units this CTA queued for replay
+  __shared__ int s_nwalk;
   __shared__ int s_i[8];
-  __shared__ long long s_l[4];
   __shared__ int s_over[kMaxDeg];
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
   __shared__ int s_defer_n;
   Counters* c = S.cnt;
   const int tid = threadIdx.x;
+  const int crank = (int)cl.block_rank();
+  const int g = crank * kUpdThreads + tid;  // cluster-wide thread index
+  const bool lead = crank == 0 && tid == 0;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int gwarp = crank * (kUpdThreads / 32) + warp;
+  int parity = 0;
   const long long t_kernel = clock64();
-  if (tid == 0) {
+  long long t_ph = t_kernel;
+  if (lead) {
     c->processed = c->discarded = c->events = c->windows = 0;
     c->inserted_start = c->next_id;
     c->stale_n = 0;
+    c->nwalk = 0;
   }
-  __syncthreads();
+  if (tid == 0) s_nwalk = 0;
+  cl.sync();
   int j0 = 0;
-  long long t_ph = clock64();
   while (j0 < m) {
-    if (tid == 0) t_ph = clock64();
-    const int wend = min(j0 + kWin, m);
+    if (lead) t_ph = clock64();
+    const int wend = min(j0 + kWinC, m);
     const int next_id = c->next_id;
     const long long tick0 = c->tick;
     const long long next_sweep = c->next_sweep;
     const int n_units = c->n_units;
     const bool iso = c->iso_count > 0;
-    // ---- A: candidates (thread owns a contiguous chunk: order-preserving compaction)
-    const int cj0 = j0 + tid * kSigPerThread;
-    unsigned cmask = 0;
-#pragma unroll
-    for (int q = 0; q < kSigPerThread; ++q) {
-      const int j = cj0 + q;
-      if (j < wend) {
-        const WinRec r = rec[j];
-        const bool cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
-                          S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
-        if (cand) {
-          cmask |= 1u << q;
-          atomicMin(&S.firstwin[r.b], j);
-        }
-      }
+    // ---- A: candidates; the first candidate per winner is processed
+    const int j = j0 + g;
+    bool cand = false;
+    int cb = -1;
+    if (j < wend) {
+      const WinRec r = rec[j];
+      cb = r.b;
+      cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
+             S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
+      if (cand) atomicMin(&S.firstwin[r.b], j);
     }
-    // minimum last_active over live units (silent-sweep test), window-start state
+    // minimum last_active over live units (silent-sweep test), window start
     long long minla = 0x7fffffffffffffffLL;
-    if (tick0 + kWin >= next_sweep) {
-      for (int u = tid; u < next_id; u += kUpdThreads) {
+    if (tick0 + kWinC >= next_sweep) {
+      for (int u = g; u < next_id; u += kWinC) {
         const long long t = S.la_val[u];
         if (t != -1 && S.alive[u] && t < minla) minla = t;
       }
     }
-    minla = block_min_ll(minla, s_ll32);  // contains __syncthreads
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
-    unsigned pmask = 0;
-#pragma unroll
-    for (int q = 0; q < kSigPerThread; ++q)
-      if ((cmask >> q) & 1u) {
-        const int j = cj0 + q;
-        if (S.firstwin[rec[j].b] == j) pmask |= 1u << q;
-      }
+    minla = cl_min_ll(minla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
+    const bool proc = cand && S.firstwin[cb] == j;
     int nproc;
-    int rank = block_excl_scan(__popc(pmask), s_warp, &nproc);
-#pragma unroll
-    for (int q = 0; q < kSigPerThread; ++q)
-      if ((pmask >> q) & 1u) s_plist[rank++] = cj0 + q;
-    __syncthreads();
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[1] += t_ - t_ph; t_ph = t_; }
-    // ---- B: events and adapt_threshold outcomes, one processed signal per thread
-    // sweep schedule inside the window: fires at ticks next_sweep + 1024 k; the
-    // k-th is silent iff cutoff_k <= 0 or every live unit's last_active >= cutoff_k
+    const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
+    if (proc) {
+      int* dst = cl.map_shared_rank(s_plist, rank / kUpdThreads);
+      dst[rank % kUpdThreads] = j;
+    }
+    cl.sync();
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[1] += t_ - t_ph; t_ph = t_; }
+    // ---- B: events and adapt_threshold outcomes; thread g owns rank g
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     int evr = 0x7fffffff;
-    for (int r = tid; r < nproc; r += kUpdThreads) {
-      const int j = s_plist[r];
-      const WinRec w = rec[j];
+    if (g < nproc) {
+      const int r = g;
+      const int jj = s_plist[tid];
+      const WinRec w = rec[jj];
       const int b = w.b, s = w.s;
       const long long tick_j = tick0 + r + 1;
       bool ev = iso;
@@ -271,9 +347,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
       }
       const int db = S.deg[b];
       const int2* B = S.adj + (size_t)b * kMaxDeg;
-      // habituation only decays (x c_b, x c_n < 1), so a unit trained at the
-      // window start is trained at any later time: the exact per-time value is
-      // reconstructed only for units still at or above h_t
+      // habituation only decays, so a unit trained at the window start stays
+      // trained: exact per-time values are replayed only for untrained units
       const double hbT = S.hab[b];
       const bool b_trained = hbT < P.h_t;
       bool found = false;
@@ -284,12 +359,12 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         const bool is_s = v == s;
         found |= is_s;
         const int age = is_s ? 0 : S.eage[ent.y];
-        const bool age_risk = !is_s && age + 2 > P.max_age;  // may exceed max_age at j
+        const bool age_risk = !is_s && age + 2 > P.max_age;
         if (!b_trained || age_risk) {
           const int jv = S.firstwin[v];
-          if (jv < j) kcn++;
+          if (jv < jj) kcn++;
           if (age_risk) {
-            const int a2 = jv < j ? ((rec[jv].s == b) ? 0 : age + 1) : age;
+            const int a2 = jv < jj ? ((rec[jv].s == b) ? 0 : age + 1) : age;
             if (a2 + 1 > P.max_age) ev = true;
           }
         }
@@ -307,15 +382,15 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
           for (int k = 0; k < db && ok; ++k) {
             const int v = B[k].x;
             const double hvT = S.hab[v];
-            if (hvT < P.h_t) continue;  // trained neighbour stays trained
+            if (hvT < P.h_t) continue;
             const int jv = S.firstwin[v];
-            const bool vwon = jv < j;
+            const bool vwon = jv < jj;
             const int dv = S.deg[v];
             const int2* V = S.adj + (size_t)v * kMaxDeg;
             int k1 = 0, k2 = 0;
             for (int q = 0; q < dv; ++q) {
               const int jw = S.firstwin[V[q].x];
-              if (jw <= j) {
+              if (jw <= jj) {
                 if (vwon && jw > jv) k2++;
                 else k1++;
               }
@@ -333,89 +408,95 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
           }
         }
       }
-      s_pat[r] = pat;
-      if (ev && r < evr) evr = r;
+      s_pat[tid] = pat;
+      // last_active presence at the window start (dict order stamps)
+      s_abs[tid] = (unsigned char)((S.la_val[b] == -1 ? 1 : 0) | (S.la_val[s] == -1 ? 2 : 0));
+      if (ev) evr = r;
     }
-    const int rstar = min(block_min(evr, s_warp), nproc);  // first event (rank)
-    const int jstar = rstar < nproc ? s_plist[rstar] : wend;
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[2] += t_ - t_ph; t_ph = t_; }
-    // ---- C: commit ranks [0, rstar)
-    for (int r = tid; r < rstar; r += kUpdThreads) {
-      const int j = s_plist[r];
-      const WinRec w = rec[j];
-      const long long tick_j = tick0 + r + 1;
-      S.claim[w.b] = batch_no;
-      if (S.la_val[w.b] == -1) atomicMin(&S.la_stamp[w.b], 3 * tick_j);
-      if (S.la_val[w.s] == -1) atomicMin(&S.la_stamp[w.s], 3 * tick_j + 1);
-      const int p = s_pat[r];
-      if (p != -2) {
-        S.patience[w.b] = p & 0x3fffffff;
-        if (p >> 30) S.theta[w.b] = dmul(S.theta[w.b], P.rho);
-      }
-      atomicMin(&S.touchfirst[w.b], j);
-      const int db = S.deg[w.b];
-      const int2* B = S.adj + (size_t)w.b * kMaxDeg;
-      for (int k = 0; k < db; ++k) atomicMin(&S.touchfirst[B[k].x], j);
+    const int rstar = min(cl_min(evr, s_warp, s_cta, parity), nproc);
+    if (tid == 0) {
+      s_i[4] = rstar < nproc ? cl.map_shared_rank(s_plist, rstar / kUpdThreads)[rstar % kUpdThreads]
+                             : wend;
     }
-    if (tid == 0) s_i[0] = 0;
     __syncthreads();
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[3] += t_ - t_ph; t_ph = t_; }
-    // last_active values after the stamps were taken from the window-start state
-    for (int r = tid; r < rstar; r += kUpdThreads) {
-      const WinRec w = rec[s_plist[r]];
-      const long long tick_j = tick0 + r + 1;
-      atomicMax(&S.la_val[w.b], tick_j);
-      atomicMax(&S.la_val[w.s], tick_j);
-    }
-    // owner list of touched units + edge-age replay
-    for (int r = tid; r < rstar; r += kUpdThreads) {
-      const int j = s_plist[r];
-      const WinRec w = rec[j];
-      const int b = w.b, s = w.s;
-      if (S.touchfirst[b] == j) S.scratch[atomicAdd(&s_i[0], 1)] = b;
-      const int db = S.deg[b];
-      const int2* B = S.adj + (size_t)b * kMaxDeg;
+    const int jstar = s_i[4];
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[2] += t_ - t_ph; t_ph = t_; }
+    // ---- C1: claims, last_active (+ order stamps), patience/threshold,
+    //      touched-unit owners, edge-age replay
+    const bool com = g < rstar;
+    WinRec cw;
+    int cj = 0;
+    if (com) {
+      cj = s_plist[tid];
+      cw = rec[cj];
+      const long long ctick = tick0 + g + 1;
+      const int absent = s_abs[tid];
+      S.claim[cw.b] = batch_no;
+      if (absent & 1) atomicMin(&S.la_stamp[cw.b], 3 * ctick);
+      if (absent & 2) atomicMin(&S.la_stamp[cw.s], 3 * ctick + 1);
+      atomicMax(&S.la_val[cw.b], ctick);
+      atomicMax(&S.la_val[cw.s], ctick);
+      const int p = s_pat[tid];
+      if (p != -2) {
+        S.patience[cw.b] = p & 0x3fffffff;
+        if (p >> 30) S.theta[cw.b] = dmul(S.theta[cw.b], P.rho);
+      }
+      // the first thread to touch a unit queues it for one replay (any thread
+      // may own it: the replay order comes from firstwin, not from the owner)
+      if (atomicExch(&S.touchfirst[cw.b], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, cw.b);
+      const int db = S.deg[cw.b];
+      const int2* B = S.adj + (size_t)cw.b * kMaxDeg;
       for (int k = 0; k < db; ++k) {
         const int2 ent = B[k];
         const int v = ent.x;
-        if (S.touchfirst[v] == j) S.scratch[atomicAdd(&s_i[0], 1)] = v;
+        if (atomicExch(&S.touchfirst[v], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, v);
         const int jv = S.firstwin[v];
-        if (jv < jstar && jv > j) continue;  // v's own signal replays this edge
+        if (jv < jstar && jv > cj) continue;  // v's own signal replays this edge
         int age = S.eage[ent.y];
-        if (jv < j) age = (rec[jv].s == b) ? 0 : age + 1;
-        age = (v == s) ? 0 : age + 1;
+        if (jv < cj) age = (rec[jv].s == cw.b) ? 0 : age + 1;
+        age = (v == cw.s) ? 0 : age + 1;
         S.eage[ent.y] = age;
       }
     }
-    __syncthreads();
-    const int nwalk = s_i[0];
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[4] += t_ - t_ph; t_ph = t_; }
-    for (int i = tid; i < nwalk; i += kUpdThreads) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
-    __syncthreads();
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[6] += t_ - t_ph; t_ph = t_; }
+    cl.sync();
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[3] += t_ - t_ph; t_ph = t_; }
+    // ---- C2: each touched unit's position / habituation sequence replayed once
+    const int nloc = min(s_nwalk, kWalkCap);
+    for (int i = tid; i < nloc; i += kUpdThreads) walk_unit(S, P, sig, s_walk[i], jstar);
+    const int nglob = c->nwalk;  // overflow list (only for very high degrees)
+    for (int i = g; i < nglob; i += kWinC) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
+    cl.sync();
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
-    if (tid == 0) {
+    if (lead) {
       c->tick = tick0 + rstar;
       c->processed += rstar;
       c->discarded += (jstar - j0) - rstar;
       c->windows++;
-      // silent sweeps that fired among the committed ticks move the clock
-      long long ns = next_sweep;
+      long long ns = next_sweep;  // silent sweeps among the committed ticks
       while (ns <= tick0 + rstar) ns += kSweepEvery;
       c->next_sweep = ns;
     }
-    for (int q = 0; q < kSigPerThread; ++q)
-      if ((cmask >> q) & 1u) S.firstwin[rec[cj0 + q].b] = kNone32;
-    for (int i = tid; i < nwalk; i += kUpdThreads) S.touchfirst[(int)S.scratch[i]] = kNone32;
-    __syncthreads();
-    // ---- D: the event signal, exactly as update_single
-    if (tid == 0) { const long long t_ = clock64(); c->cyc_phase[7] += t_ - t_ph; t_ph = t_; }
+    if (cand) S.firstwin[cb] = kNone32;
+    for (int i = tid; i < nloc; i += kUpdThreads) S.touchfirst[s_walk[i]] = kNone32;
+    for (int i = g; i < nglob; i += kWinC) S.touchfirst[(int)S.scratch[i]] = kNone32;
+    cl.sync();
+    if (tid == 0) s_nwalk = 0;
+    if (lead) {
+      c->nwalk = 0;
+      const long long t_ = clock64();
+      c->cyc_phase[7] += t_ - t_ph;
+      t_ph = t_;
+    }
+    // ---- D: the event signal, exactly as update_single (CTA 0)
     if (rstar < nproc) {
       const long long t_ser = clock64();
-      const int warp = tid >> 5, lane = tid & 31;
-      if (tid == 0) s_defer_n = 0;
+      if (lead) {
+        s_defer_n = 0;
+        c->defer_n = 0;
+      }
       __syncthreads();
-      if (warp == 0) {
+      if (crank == 0 && warp == 0) {
         DevState SD = S;
         SD.defer_n = &s_defer_n;
         const WinRec r = rec[jstar];
@@ -429,8 +510,7 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
           c->stale_n = 0;
         }
         __syncwarp();
-        // winner and its neighbours move / decay: independent units, one lane each
-        // (engine.py:316-329)
+        // winner and neighbours move / decay: independent units, one lane each
         if (lane == 0) {
           double4 p = S.pos[r.b];
           move_toward(p, P.eps_b, x, y, z);
@@ -453,16 +533,17 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
         __syncwarp();
         if (lane == 0) {
           const int fired = event_part1b(SD, P, r.b, r.s, r.dwin, x, y, z, s_over, s_i[3]);
-          s_i[1] = fired;
-          s_l[0] = fired ? sweep_cutoff(S, P) : 0;
-          s_i[2] = r.b;
+          c->ev_fired = fired;
+          c->ev_cutoff = fired ? sweep_cutoff(S, P) : 0;
+          c->ev_b = r.b;
+          c->defer_n = s_defer_n;
         }
       }
-      __syncthreads();
-      // deferred ring reclassification, one warp per affected unit
+      cl.sync();
+      // deferred ring reclassification, one warp per affected unit (cluster-wide)
       {
-        const int nd = min(s_defer_n, kDeferCap);
-        for (int i = warp; i < nd; i += 32) {
+        const int nd = min(c->defer_n, kDeferCap);
+        for (int i = gwarp; i < nd; i += kCluster * (kUpdThreads / 32)) {
           const int u = S.defer_list[i];
           if (S.alive[u]) {
             const int nw = classify_ring_warp(S, u, s_ring_sh[warp]);
@@ -478,12 +559,11 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
           if (lane == 0) S.touchfirst[u] = kNone32;
         }
       }
-      __syncthreads();
-      const int fired = s_i[1];
-      const long long cutoff = s_l[0];
+      const int fired = c->ev_fired;
+      const long long cutoff = c->ev_cutoff;
       if (fired && cutoff > 0) {
         const int nid = c->next_id;
-        for (int u = tid; u < nid; u += kUpdThreads) {
+        for (int u = g; u < nid; u += kWinC) {
           const long long t = S.la_val[u];
           if (t != -1 && t < cutoff) {
             const int q = atomicAdd(&c->stale_n, 1);
@@ -492,19 +572,19 @@ __global__ void __launch_bounds__(kUpdThreads, 1)
           }
         }
       }
-      __syncthreads();
-      if (tid == 0) {
-        serial_update_part2(S, P, s_i[2], c->stale_n, fired != 0);
+      cl.sync();
+      if (lead) {
+        serial_update_part2(S, P, c->ev_b, c->stale_n, fired != 0);
         c->cyc_serial += clock64() - t_ser;
       }
-      __syncthreads();
+      cl.sync();
       j0 = jstar + 1;
     } else {
       j0 = wend;
     }
-    __syncthreads();
   }
-  // compact rows when dead entries exceed 1/8 (keeps id order)
+  if (crank != 0) return;
+  // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
   if (c->ndead_rows * 8 > c->nrows) {
     const int n = c->nrows;
     int out = 0;
