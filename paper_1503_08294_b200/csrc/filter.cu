@@ -1,9 +1,576 @@
-// filter.cu -- FP32 filter + certified FP64 re-check for the find (placeholder:
-// the exact path runs until the filter lands).
+// filter.cu -- FP32 find-winners filter with a certified FP64 re-check (sm_100a).
+//
+// Output is bit-identical to the exact path (find.cu) and so to the reference
+// scan_best_two_into (pkg/src/growsurf/kernels/_scan.pyx:39-98): rows of the
+// lexicographic (d2, row) best two, d2 = ((dx*dx + dy*dy) + dz*dz) in binary64.
+//
+// Pipeline (all on one stream, no host synchronisation):
+//   1 k_bbox      bounding box of the live rows -> centre c (an FP32 value).
+//   2 k_prep      every row r -> P = p - c, stored as FP32 "unit pairs"
+//                 {-2Px, -2Py, -2Pz, |P|^2} for rows (2i, 2i+1) and
+//                 Pmax = max |P| (rounded up).  Dead rows get |P|^2 = +inf.
+//   3 k_filter    per signal Q = q - c in FP32 registers; for every unit
+//                 e = |P|^2 - 2 P.Q (= d - |Q|^2) with three packed FFMA2
+//                 per two units; keeps the lexicographic (e, row) top-3.
+//                 Unit tiles are streamed into shared memory by TMA bulk
+//                 copies (cp.async.bulk + mbarrier, double-buffered) and
+//                 read as broadcasts.  Split over unit chunks when m alone
+//                 cannot fill the GPU; k_filter_merge merges the partial
+//                 top-3s in chunk (= row) order.
+//   4 certify     the two FP32 candidates are re-evaluated EXACTLY (FP64,
+//                 reference rounding).  They are the exact top-2 if every
+//                 other unit is provably farther: with E = 8u(Pmax+|Q|)^2
+//                 bounding |e_fp32 - e_real| (u = 2^-24; derivation in
+//                 DESIGN.md), every non-candidate has
+//                 d_real >= e3 - E + |Q|^2, and we require that bound to
+//                 exceed both candidates' FP64 distances with margin for
+//                 the FP64 roundings.  Otherwise the signal is appended to
+//                 a fallback list.
+//   5 k_fallback  one CTA per listed signal scans all rows in FP64 (exact
+//                 reference arithmetic) and reduces the lexicographic top-2.
+//
+// Algorithmic work: 8 FLOP per (signal, unit) pair as in the reference
+// (3 sub, 3 mul, 2 add); this kernel issues 3 FMA lanes per pair.
+
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gs {
 
-bool find_filter_launch(Ctx&, const FindArgs&, cudaStream_t, DevBuf&) { return false; }
+constexpr int kQT = 256;           // threads per filter CTA
+constexpr int kQS = 4;             // signals per thread
+constexpr int kSigPerCta = kQT * kQS;
+constexpr int kTilePairs = 512;    // unit pairs (1024 units) per shared-memory tile
+constexpr int kFbThreads = 256;    // fallback CTA
+constexpr int kMinChunkTiles = 2;  // fewest tiles per split-n chunk
+
+struct __align__(16) UPair {
+  float ax0, ax1, ay0, ay1;  // -2 P.x, -2 P.y for rows 2i, 2i+1
+  float az0, az1, w0, w1;    // -2 P.z, |P|^2
+};
+
+struct FilterMeta {
+  unsigned long long bbox[6];  // ordered-int encoded min x,y,z / max x,y,z
+  double cx, cy, cz;           // centre (FP32-representable)
+  unsigned int pmax_bits;      // float bits of max |P| (rounded up)
+  unsigned int nfb;            // fallback list length
+  unsigned int nlive;          // live rows scanned
+};
+
+struct Top3 {
+  float e1, e2, e3;
+  int32_t i1, i2, i3;
+};
+
+__device__ __forceinline__ unsigned long long ord_enc(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ord_dec(unsigned long long k) {
+  const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k;
+  return __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ bool filter_row(const FindArgs& a, int64_t nrows, int64_t r, double& x,
+                                           double& y, double& z) {
+  if (r >= nrows) return false;
+  if (a.pos4) {
+    const int32_t slot = a.rows ? a.rows[r] : (int32_t)r;
+    if (a.alive && !a.alive[slot]) return false;
+    const double4 p = a.pos4[slot];
+    x = p.x;
+    y = p.y;
+    z = p.z;
+    return true;
+  }
+  x = a.pos[3 * r];
+  y = a.pos[3 * r + 1];
+  z = a.pos[3 * r + 2];
+  return true;
+}
+
+__device__ __forceinline__ int64_t rows_of(const FindArgs& a) {
+  return a.n_dev ? (int64_t)*a.n_dev : a.n;
+}
+
+__global__ void k_filter_init(FilterMeta* M) {
+  if (threadIdx.x < 3) {
+    M->bbox[threadIdx.x] = ~0ULL;
+    M->bbox[3 + threadIdx.x] = 0ULL;
+  }
+  if (threadIdx.x == 0) {
+    M->pmax_bits = 0u;
+    M->nfb = 0u;
+    M->nlive = 0u;
+  }
+}
+
+__global__ void k_bbox(FindArgs a, FilterMeta* M) {
+  const int64_t nrows = rows_of(a);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double p[3];
+    if (!filter_row(a, nrows, r, p[0], p[1], p[2])) continue;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fmin(lo[k], p[k]);
+      hi[k] = fmax(hi[k], p[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (lo[k] <= hi[k]) {
+        atomicMin(&M->bbox[k], ord_enc(lo[k]));
+        atomicMax(&M->bbox[3 + k], ord_enc(hi[k]));
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void centre_of(const FilterMeta* M, double& cx, double& cy, double& cz) {
+  double c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const unsigned long long lo = M->bbox[k], hi = M->bbox[3 + k];
+    c[k] = (lo == ~0ULL) ? 0.0 : (double)__double2float_rn(0.5 * (ord_dec(lo) + ord_dec(hi)));
+  }
+  cx = c[0];
+  cy = c[1];
+  cz = c[2];
+}
+
+// rows -> FP32 unit pairs (npairs_alloc pairs; rows past the live count are +inf)
+__global__ void k_prep(FindArgs a, FilterMeta* M, UPair* U, int64_t npairs_alloc) {
+  const int64_t nrows = rows_of(a);
+  double cx, cy, cz;
+  centre_of(M, cx, cy, cz);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    M->cx = cx;
+    M->cy = cy;
+    M->cz = cz;
+  }
+  float pm = 0.f;
+  unsigned live = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npairs_alloc;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float ax[2], ay[2], az[2], w[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double x, y, z;
+      if (filter_row(a, nrows, 2 * i + h, x, y, z)) {
+        const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
+                    pz = __double2float_rn(z - cz);
+        ax[h] = -2.f * px;
+        ay[h] = -2.f * py;
+        az[h] = -2.f * pz;
+        const double n2 = (double)px * px + (double)py * py + (double)pz * pz;
+        w[h] = __double2float_rn(n2);
+        const double dx = x - cx, dy = y - cy, dz = z - cz;
+        pm = fmaxf(pm, __double2float_ru(sqrt(dx * dx + dy * dy + dz * dz)));
+        ++live;
+      } else {
+        ax[h] = ay[h] = az[h] = 0.f;
+        w[h] = INFINITY;
+      }
+    }
+    UPair u;
+    u.ax0 = ax[0];
+    u.ax1 = ax[1];
+    u.ay0 = ay[0];
+    u.ay1 = ay[1];
+    u.az0 = az[0];
+    u.az1 = az[1];
+    u.w0 = w[0];
+    u.w1 = w[1];
+    U[i] = u;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    live += __shfl_xor_sync(0xffffffffu, live, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (pm > 0.f) atomicMax(&M->pmax_bits, __float_as_uint(pm));
+    if (live) atomicAdd(&M->nlive, live);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk copy + mbarrier helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void top3_push(Top3& t, float e, int32_t r) {
+  if (e < t.e3) {
+    if (e < t.e2) {
+      t.e3 = t.e2;
+      t.i3 = t.i2;
+      if (e < t.e1) {
+        t.e2 = t.e1;
+        t.i2 = t.i1;
+        t.e1 = e;
+        t.i1 = r;
+      } else {
+        t.e2 = e;
+        t.i2 = r;
+      }
+    } else {
+      t.e3 = e;
+      t.i3 = r;
+    }
+  }
+}
+
+__device__ __forceinline__ void top3_init(Top3& t) {
+  t.e1 = t.e2 = t.e3 = INFINITY;
+  t.i1 = t.i2 = t.i3 = -1;
+}
+
+// FP64 reference distance of row r (dead rows: +inf, never selected)
+__device__ __forceinline__ double exact_d2(const FindArgs& a, int64_t nrows, int32_t r, double qx,
+                                           double qy, double qz) {
+  double x, y, z;
+  if (!filter_row(a, nrows, r, x, y, z)) return INFINITY;
+  return dist2_exact(x, y, z, qx, qy, qz);
+}
+
+__device__ __forceinline__ void write_best(const FindArgs& a, int64_t j, const Best2& b) {
+  if (a.out_idx) {
+    a.out_idx[2 * j] = b.i1;
+    a.out_idx[2 * j + 1] = b.i2;
+    a.out_d2[2 * j] = b.d1;
+    a.out_d2[2 * j + 1] = b.d2;
+  }
+  if (a.out_win) {
+    WinRec w;
+    w.b = (b.i1 >= 0 && a.rows) ? a.rows[b.i1] : b.i1;
+    w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
+    w.dwin = __dsqrt_rn(b.d1);  // math.sqrt: multi.py:72-78
+    a.out_win[j] = w;
+  }
+}
+
+// Certify the FP32 top-3 of signal j and write its exact result, or list it
+// for the exact fallback scan.
+__device__ void certify(const FindArgs& a, const FilterMeta* M, int64_t j, const Top3& t,
+                        int32_t* fb_list) {
+  const int64_t nrows = rows_of(a);
+  const double qx = a.sig[3 * j], qy = a.sig[3 * j + 1], qz = a.sig[3 * j + 2];
+  Best2 b;
+  b.init();
+  // candidates in row order so strict-< gives the lexicographic (d, row) order
+  int32_t c0 = t.i1, c1 = t.i2;
+  if (c1 >= 0 && c1 < c0) {
+    const int32_t tmp = c0;
+    c0 = c1;
+    c1 = tmp;
+  }
+  double d0 = INFINITY, d1 = INFINITY;
+  if (c0 >= 0) b.push(d0 = exact_d2(a, nrows, c0, qx, qy, qz), c0);
+  if (c1 >= 0) b.push(d1 = exact_d2(a, nrows, c1, qx, qy, qz), c1);
+  const double Qx = qx - M->cx, Qy = qy - M->cy, Qz = qz - M->cz;
+  const double q2 = Qx * Qx + Qy * Qy + Qz * Qz;
+  const double R = (double)__uint_as_float(M->pmax_bits) + sqrt(q2);
+  const double R2 = R * R;
+  // e stays far from FP32 overflow below R2 = 1e30; beyond it, go exact
+  bool ok = R2 <= 1e30;
+  if (t.i3 < 0) {
+    // fewer than three finite FP32 values: certified only if every live
+    // row is among the candidates
+    ok = ok && M->nlive == (unsigned)((c0 >= 0) + (c1 >= 0));
+  } else if (ok) {
+    // |e_fp32 - e_real| <= E for every unit; 1e-44 covers
+    // FP32 subnormal rounding, which is absolute rather than relative
+    const double E = 8.0 * 0x1p-24 * R2 * (1.0 + 1e-6) + 1e-44;
+    // lower bound (real arithmetic) on d of any unit outside {c0, c1},
+    // less the FP64 rounding slack of q2 and of the reference d values
+    const double lower = ((double)t.e3 - E + q2 - 1e-13 * R2) * (1.0 - 1e-14);
+    const double hi = fmax(d0, d1);
+    ok = (b.i2 >= 0) && lower > hi;
+  }
+  if (ok) {
+    write_best(a, j, b);
+  } else {
+    const unsigned k = atomicAdd((unsigned*)&((FilterMeta*)M)->nfb, 1u);
+    fb_list[k] = (int32_t)j;
+  }
+}
+
+// The FP32 filter: grid (signal tiles, unit chunks)
+__global__ void __launch_bounds__(kQT, 3)
+    k_filter(FindArgs a, const FilterMeta* __restrict__ M, const UPair* __restrict__ U,
+             int64_t npairs, int64_t pairs_per_chunk, Top3* __restrict__ part,
+             int32_t* __restrict__ fb_list) {
+  __shared__ __align__(128) UPair tile[2][kTilePairs];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int64_t sig0 = (int64_t)blockIdx.x * kSigPerCta;
+  const int64_t p_begin = (int64_t)blockIdx.y * pairs_per_chunk;
+  const int64_t p_end = min(npairs, p_begin + pairs_per_chunk);
+  const int ntiles = (int)((p_end - p_begin + kTilePairs - 1) / kTilePairs);
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int t) {
+    const int64_t p0 = p_begin + (int64_t)t * kTilePairs;
+    const int cnt = (int)min((int64_t)kTilePairs, p_end - p0);
+    const uint32_t bytes = (uint32_t)cnt * (uint32_t)sizeof(UPair);
+    mbar_expect_tx(&bar[t & 1], bytes);
+    tma_bulk_g2s(&tile[t & 1][0], U + p0, bytes, &bar[t & 1]);
+  };
+  if (tid == 0) {
+    if (ntiles > 0) issue(0);
+    if (ntiles > 1) issue(1);
+  }
+
+  const double cx = M->cx, cy = M->cy, cz = M->cz;
+  float2 qx[kQS], qy[kQS], qz[kQS];
+  Top3 t[kQS];
+#pragma unroll
+  for (int k = 0; k < kQS; ++k) {
+    const int64_t j = sig0 + tid + k * kQT;
+    top3_init(t[k]);
+    float x = 0.f, y = 0.f, z = 0.f;
+    if (j < a.m) {
+      x = __double2float_rn(a.sig[3 * j] - cx);
+      y = __double2float_rn(a.sig[3 * j + 1] - cy);
+      z = __double2float_rn(a.sig[3 * j + 2] - cz);
+    }
+    qx[k] = make_float2(x, x);
+    qy[k] = make_float2(y, y);
+    qz[k] = make_float2(z, z);
+  }
+
+  for (int ti = 0; ti < ntiles; ++ti) {
+    const int buf = ti & 1;
+    mbar_wait(&bar[buf], (uint32_t)((ti >> 1) & 1));
+    const int64_t p0 = p_begin + (int64_t)ti * kTilePairs;
+    const int cnt = (int)min((int64_t)kTilePairs, p_end - p0);
+    const UPair* T = tile[buf];
+    const int32_t row0 = (int32_t)(2 * p0);
+#pragma unroll 2
+    for (int i = 0; i < cnt; ++i) {
+      const float4 v0 = *reinterpret_cast<const float4*>(&T[i].ax0);
+      const float4 v1 = *reinterpret_cast<const float4*>(&T[i].az0);
+      const float2 ax = make_float2(v0.x, v0.y), ay = make_float2(v0.z, v0.w);
+      const float2 az = make_float2(v1.x, v1.y), w = make_float2(v1.z, v1.w);
+      // one predicate over all kQS signals keeps the common path branch-free
+      float2 e[kQS];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < kQS; ++k) {
+        e[k] = __ffma2_rn(ax, qx[k], w);
+        e[k] = __ffma2_rn(ay, qy[k], e[k]);
+        e[k] = __ffma2_rn(az, qz[k], e[k]);
+        any |= fminf(e[k].x, e[k].y) < t[k].e3;
+      }
+      if (any) {
+        const int32_t r = row0 + 2 * i;
+#pragma unroll
+        for (int k = 0; k < kQS; ++k) {
+          top3_push(t[k], e[k].x, r);
+          top3_push(t[k], e[k].y, r + 1);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this buffer
+    if (tid == 0 && ti + 2 < ntiles) issue(ti + 2);
+  }
+
+#pragma unroll
+  for (int k = 0; k < kQS; ++k) {
+    const int64_t j = sig0 + tid + k * kQT;
+    if (j >= a.m) continue;
+    if (part)
+      part[(int64_t)blockIdx.y * a.m + j] = t[k];
+    else
+      certify(a, M, j, t[k], fb_list);
+  }
+}
+
+__global__ void k_filter_merge(FindArgs a, const FilterMeta* M, int nchunks, const Top3* part,
+                               int32_t* fb_list) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.m) return;
+  Top3 t;
+  top3_init(t);
+  for (int c = 0; c < nchunks; ++c) {
+    const Top3 p = part[(int64_t)c * a.m + j];
+    if (p.i1 >= 0) top3_push(t, p.e1, p.i1);
+    if (p.i2 >= 0) top3_push(t, p.e2, p.i2);
+    if (p.i3 >= 0) top3_push(t, p.e3, p.i3);
+  }
+  certify(a, M, j, t, fb_list);
+}
+
+// lexicographic (d, row) merge of two best-two records
+__device__ __forceinline__ void best2_merge(Best2& b, double d, int32_t i) {
+  if (i < 0) return;
+  if (d < b.d1 || (d == b.d1 && i < b.i1)) {
+    b.d2 = b.d1;
+    b.i2 = b.i1;
+    b.d1 = d;
+    b.i1 = i;
+  } else if (i != b.i1 && (d < b.d2 || (d == b.d2 && i < b.i2))) {
+    b.d2 = d;
+    b.i2 = i;
+  }
+}
+
+// exact FP64 scan for listed signals: one CTA per signal (persistent)
+__global__ void __launch_bounds__(kFbThreads) k_fallback(FindArgs a, const FilterMeta* M,
+                                                         const int32_t* fb_list) {
+  __shared__ double s_d[2][kFbThreads / 32];
+  __shared__ int32_t s_i[2][kFbThreads / 32];
+  const int64_t nrows = rows_of(a);
+  const unsigned nfb = M->nfb;
+  for (unsigned f = blockIdx.x; f < nfb; f += gridDim.x) {
+    const int64_t j = fb_list[f];
+    const double qx = a.sig[3 * j], qy = a.sig[3 * j + 1], qz = a.sig[3 * j + 2];
+    Best2 b;
+    b.init();
+    for (int64_t r = threadIdx.x; r < nrows; r += kFbThreads) {
+      double x, y, z;
+      if (!filter_row(a, nrows, r, x, y, z)) continue;
+      b.push(dist2_exact(x, y, z, qx, qy, qz), (int32_t)r);  // rows ascend per thread
+    }
+    // warp reduction (lexicographic: order-independent)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od1 = __shfl_xor_sync(0xffffffffu, b.d1, o);
+      const double od2 = __shfl_xor_sync(0xffffffffu, b.d2, o);
+      const int32_t oi1 = __shfl_xor_sync(0xffffffffu, b.i1, o);
+      const int32_t oi2 = __shfl_xor_sync(0xffffffffu, b.i2, o);
+      best2_merge(b, od1, oi1);
+      best2_merge(b, od2, oi2);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      s_d[0][w] = b.d1;
+      s_d[1][w] = b.d2;
+      s_i[0][w] = b.i1;
+      s_i[1][w] = b.i2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Best2 r;
+      r.init();
+      for (int k = 0; k < kFbThreads / 32; ++k) {
+        best2_merge(r, s_d[0][k], s_i[0][k]);
+        best2_merge(r, s_d[1][k], s_i[1][k]);
+      }
+      write_best(a, j, r);
+    }
+    __syncthreads();
+  }
+}
+
+static int g_filter_ctas_per_sm = 0;
+
+bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work) {
+  if (a.m <= 0) return true;
+  // AUTO: the filter pays for its extra passes only on large scans
+  if (a.mode == GS_FIND_AUTO && (a.n < 4096 || (double)a.n * (double)a.m < 6.0e7)) return false;
+  if (a.n < 3) return false;
+  if (g_filter_ctas_per_sm == 0) {
+    int occ = 0;
+    GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_filter, kQT, 0));
+    g_filter_ctas_per_sm = std::max(1, occ);
+  }
+  const int64_t npairs = (a.n + 1) / 2;
+  const int64_t gx = (a.m + kSigPerCta - 1) / kSigPerCta;
+  const int64_t ntiles_total = (npairs + kTilePairs - 1) / kTilePairs;
+  // split-n: pick the chunk count whose wave quantisation wastes least
+  const double resident = (double)ctx.sm_count * g_filter_ctas_per_sm;
+  int64_t best_c = 1;
+  double best_eff = -1.0;
+  const int64_t max_c = std::max<int64_t>(1, std::min<int64_t>(64, ntiles_total / kMinChunkTiles));
+  for (int64_t c = 1; c <= max_c; ++c) {
+    const double waves = (double)(gx * c) / resident;
+    const double eff = waves / std::ceil(waves) * (waves >= 2.0 ? 1.0 : 0.5 + 0.25 * waves);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best_c = c;
+    }
+  }
+  const int64_t tiles_per_chunk = (ntiles_total + best_c - 1) / best_c;
+  const int64_t pairs_per_chunk = tiles_per_chunk * kTilePairs;
+  const int64_t nchunks = (npairs + pairs_per_chunk - 1) / pairs_per_chunk;
+
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t meta_b = al(sizeof(FilterMeta));
+  const size_t pair_b = al(sizeof(UPair) * (size_t)npairs);
+  const size_t fb_b = al(sizeof(int32_t) * (size_t)a.m);
+  const size_t part_b = nchunks > 1 ? al(sizeof(Top3) * (size_t)nchunks * (size_t)a.m) : 0;
+  char* base = (char*)work.get(meta_b + pair_b + fb_b + part_b);
+  FilterMeta* M = (FilterMeta*)base;
+  UPair* U = (UPair*)(base + meta_b);
+  int32_t* fb = (int32_t*)(base + meta_b + pair_b);
+  Top3* part = nchunks > 1 ? (Top3*)(base + meta_b + pair_b + fb_b) : nullptr;
+
+  const int prep_grid = (int)std::min<int64_t>(4LL * ctx.sm_count, (npairs + 255) / 256 + 1);
+  k_filter_init<<<1, 32, 0, stream>>>(M);
+  k_bbox<<<prep_grid, 256, 0, stream>>>(a, M);
+  k_prep<<<prep_grid, 256, 0, stream>>>(a, M, U, npairs);
+  dim3 grid((unsigned)gx, (unsigned)nchunks);
+  k_filter<<<grid, kQT, 0, stream>>>(a, M, U, npairs, pairs_per_chunk, part, fb);
+  if (nchunks > 1)
+    k_filter_merge<<<(unsigned)((a.m + 255) / 256), 256, 0, stream>>>(a, M, (int)nchunks, part, fb);
+  k_fallback<<<ctx.sm_count * 8, kFbThreads, 0, stream>>>(a, M, fb);
+  GS_CUDA(cudaGetLastError());
+  g_launches += 5 + (nchunks > 1 ? 1 : 0);
+  // fallback count for gs_find_last_fallbacks (device-to-device, stays async)
+  if (!ctx.d_fallbacks) GS_CUDA(cudaMalloc(&ctx.d_fallbacks, sizeof(unsigned long long)));
+  GS_CUDA(cudaMemsetAsync(ctx.d_fallbacks, 0, sizeof(unsigned long long), stream));
+  GS_CUDA(cudaMemcpyAsync(ctx.d_fallbacks, &M->nfb, sizeof(unsigned), cudaMemcpyDeviceToDevice,
+                          stream));
+  return true;
+}
 
 }  // namespace gs

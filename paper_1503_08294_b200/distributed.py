@@ -26,6 +26,20 @@ def shard_bounds(m: int, world: int, rank: int) -> tuple[int, int]:
     return rank * m // world, (rank + 1) * m // world
 
 
+def gather_records(full, lo: int, hi: int, group=None):
+    """All-gather every rank's record slice [lo, hi) of ``full`` (a uint8
+    tensor of m * REC_BYTES bytes) into ``full`` in rank order == batch order.
+
+    Works for any torch.distributed backend (NCCL on the GPU path, gloo in
+    the CPU tests); slices must be equal-sized (m divisible by the world).
+    """
+    import torch.distributed as dist
+
+    local = full[lo * REC_BYTES: hi * REC_BYTES].clone()
+    dist.all_gather_into_tensor(full, local, group=group)
+    return full
+
+
 class ShardedStep:
     """find(slice) -> all_gather(records) -> replicated update, per batch."""
 
@@ -58,11 +72,9 @@ class ShardedStep:
         lib = _lib.load_library()
         full = self._buffers(m)
         lo, hi = shard_bounds(m, self.world, self.rank)
-        chunk = (hi - lo) * REC_BYTES
         with self.torch.cuda.stream(self.stream):
             _lib.check(lib.gs_engine_find_device(self.net.handle, d_sig, lo, hi, full.data_ptr()))
-            local = full[lo * REC_BYTES: lo * REC_BYTES + chunk].clone()
-            self.dist.all_gather_into_tensor(full, local, group=self.group)
+            gather_records(full, lo, hi, self.group)
             _lib.check(lib.gs_engine_update_device(self.net.handle, d_sig, m, full.data_ptr()))
 
 
