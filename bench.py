@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
+    p.add_argument("--no-find-microbench", action="store_true")
     return p.parse_args()
 
 
@@ -272,6 +273,87 @@ def ncu_traffic(kernel: str):
         return None
 
 
+def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000), m=1_000_000,
+                    reps=3, cpu_budget_s=8.0):
+    """BASELINE config 5: m = 1e6 signals vs n units, uniform [0,1)^3 from
+    Philox(7) (cli.py:252-261).  Resident inputs, FP32 filter + certified
+    FP64 re-check (bit-identical to the reference scan), CUDA events on the
+    launching stream, L2 flushed between repetitions (the unit-pair array of
+    the largest n is 16 MB; signals 24 MB)."""
+    import numpy as np
+    import torch
+
+    out = {"m": m, "mode": "filter (FP32 FFMA2 + certified FP64)", "lines": []}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.Stream()  # a real stream: handle 0 would mean the context's own stream
+    peak = 2 * 128 * ctx.sm_count * sm_mhz * 1e6 / 1e12
+    for n in sizes:
+        rng = np.random.Generator(np.random.Philox(7))
+        pos = torch.from_numpy(rng.random((n, 3))).cuda()
+        sig = torch.from_numpy(rng.random((m, 3))).cuda()
+        idx = torch.empty((m, 2), dtype=torch.int64, device="cuda")
+        d2 = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+
+        def run():
+            _lib_check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(), m,
+                                          idx.data_ptr(), d2.data_ptr(), 1, st.cuda_stream))
+
+        run()
+        times = []
+        for _ in range(reps):
+            with torch.cuda.stream(st):
+                flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            run()
+            e1.record(st)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        fb = C.c_int64()
+        _lib_check(lib.gs_find_last_fallbacks(ctx.handle, C.byref(fb)))
+        ms = statistics.median(times)
+        pairs = float(n) * m
+        achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
+        out["lines"].append({"n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),
+                             "achieved_tflops": achieved, "peak_tflops": peak,
+                             "frac": achieved / peak, "fallback_signals": fb.value})
+        del pos, sig, idx, d2
+    out["peak_source"] = (f"nominal FP32 2x128 lanes x {ctx.sm_count} SMs at the sampled "
+                          f"{sm_mhz:.0f} MHz; 8 FLOP per pair (BASELINE.md 2)")
+    # the reference's raw scan (_parallel_scan, all host cores) on a bounded sample
+    if reference_available():
+        from growsurf import kernels as rk
+        from growsurf.network import Snapshot
+        from growsurf.parallel import ExecConfig, _parallel_scan
+        import numpy as np
+
+        n = sizes[0]
+        rng = np.random.Generator(np.random.Philox(7))
+        pos = rng.random((n, 3))
+        sig = rng.random((m, 3))
+        snap = Snapshot(np.arange(n, dtype=np.int64), pos)
+        cfg = ExecConfig(workers=os.cpu_count() or 1, tile=1024)
+        ms_sig = 4096
+        t0 = time.perf_counter()
+        done = 0
+        while time.perf_counter() - t0 < cpu_budget_s and done + ms_sig <= m:
+            _parallel_scan(snap, sig[done:done + ms_sig], cfg, backend=rk.get_backend("compiled"))
+            done += ms_sig
+        sec = time.perf_counter() - t0
+        out["cpu_reference"] = {"pairs_per_s": float(n) * done / sec, "n": n, "signals": done,
+                                "cores": os.cpu_count(), "seconds": sec,
+                                "how": "growsurf.parallel._parallel_scan, compiled backend, tile 1024"}
+    return out
+
+
+def _lib_check(rc):
+    from paper_1503_08294_b200 import _lib
+
+    _lib.check(rc)
+
+
 def run_b200_arm(args):
     import numpy as np
     import torch
@@ -431,6 +513,11 @@ def run_b200_arm(args):
                "sample": f"first {sig:,} signals ({batches} batches) of the same seeded "
                          f"{args.workload} run ({sec:.1f} s)"}
 
+    fmb = None
+    if rank == 0 and not args.no_find_microbench:
+        fmb = find_microbench(lib, _lib.default_context(),
+                              clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0), peaks)
+
     if rank == 0:
         sig, conv, units, edges = result
         line = {
@@ -453,6 +540,7 @@ def run_b200_arm(args):
             "gpu_launches": int(launches),
             "clocks": clk,
             "phase_ms_per_step": {"find": find_ms, "update": update_ms},
+            "find_microbench": fmb,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

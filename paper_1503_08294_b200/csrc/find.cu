@@ -140,6 +140,85 @@ __global__ void find_merge_kernel(FindArgs a, int nchunks, const Part* part) {
   write_result(a, j, b);
 }
 
+// ---------------------------------------------------------------------------
+// Small-n exact find (the engine's regime: a few thousand units): one kernel,
+// no partial buffer.  Every CTA stages ALL rows in shared memory (24 B per
+// row) and owns 16*FS signals; the 16 lanes of a half-warp split the rows of
+// one signal (lane l scans rows l, l+16, ..., ascending) and merge their
+// best-two lexicographically on (d2, row) with xor shuffles -- the result is
+// the same for any split.
+
+constexpr int kSmallThreads = 256;
+constexpr int kSmallSlices = 16;
+constexpr int kSmallMaxRows = 6144;  // 144 KB of shared memory
+
+__device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
+  if (i < 0) return;
+  if (d < b.d1 || (d == b.d1 && i < b.i1)) {
+    b.d2 = b.d1;
+    b.i2 = b.i1;
+    b.d1 = d;
+    b.i1 = i;
+  } else if (i != b.i1 && (d < b.d2 || (d == b.d2 && i < b.i2))) {
+    b.d2 = d;
+    b.i2 = i;
+  }
+}
+
+template <int kFS>
+__global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a) {
+  extern __shared__ double s_rows[];  // [3][nr]
+  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const int nr = (int)n;
+  double* sx = s_rows;
+  double* sy = s_rows + nr;
+  double* sz = s_rows + 2 * nr;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int r = threadIdx.x; r < nr; r += kSmallThreads) {
+    double x = kInf, y = kInf, z = kInf;
+    if (!load_row(a, r, x, y, z)) x = y = z = kInf;
+    sx[r] = x;
+    sy[r] = y;
+    sz[r] = z;
+  }
+  __syncthreads();
+  const int slice = threadIdx.x & (kSmallSlices - 1);
+  const int sl = threadIdx.x / kSmallSlices;  // 0..15
+  const int64_t sig0 = (int64_t)blockIdx.x * (kSmallThreads / kSmallSlices) * kFS;
+  double qx[kFS], qy[kFS], qz[kFS];
+  Best2 b[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + sl + k * (kSmallThreads / kSmallSlices);
+    b[k].init();
+    qx[k] = qy[k] = qz[k] = 0.0;
+    if (j < a.m) {
+      qx[k] = a.sig[3 * j];
+      qy[k] = a.sig[3 * j + 1];
+      qz[k] = a.sig[3 * j + 2];
+    }
+  }
+  for (int r = slice; r < nr; r += kSmallSlices) {
+    const double px = sx[r], py = sy[r], pz = sz[r];
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) b[k].push(dist2_exact(px, py, pz, qx[k], qy[k], qz[k]), r);
+  }
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+#pragma unroll
+    for (int o = kSmallSlices / 2; o > 0; o >>= 1) {
+      const double od1 = __shfl_xor_sync(0xffffffffu, b[k].d1, o);
+      const double od2 = __shfl_xor_sync(0xffffffffu, b[k].d2, o);
+      const int32_t oi1 = __shfl_xor_sync(0xffffffffu, b[k].i1, o);
+      const int32_t oi2 = __shfl_xor_sync(0xffffffffu, b[k].i2, o);
+      best2_lex(b[k], od1, oi1);
+      best2_lex(b[k], od2, oi2);
+    }
+    const int64_t j = sig0 + sl + k * (kSmallThreads / kSmallSlices);
+    if (slice == 0 && j < a.m) write_result(a, j, b[k]);
+  }
+}
+
 // forward declaration (filter.cu)
 bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 
@@ -148,6 +227,28 @@ void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work)
   if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
       find_filter_launch(ctx, a, stream, work))
     return;
+  if (a.n <= kSmallMaxRows) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      const int bytes = 24 * kSmallMaxRows;
+      GS_CUDA(cudaFuncSetAttribute(find_small_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      GS_CUDA(cudaFuncSetAttribute(find_small_kernel<4>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      attr_set = true;
+    }
+    const size_t smem = 24 * (size_t)std::max<int64_t>(a.n, 1);
+    const int64_t per1 = kSmallThreads / kSmallSlices;
+    if (a.m >= 8LL * ctx.sm_count * per1 * 4) {
+      find_small_kernel<4><<<(unsigned)((a.m + 4 * per1 - 1) / (4 * per1)), kSmallThreads, smem,
+                             stream>>>(a);
+    } else {
+      find_small_kernel<1><<<(unsigned)((a.m + per1 - 1) / per1), kSmallThreads, smem, stream>>>(a);
+    }
+    GS_CUDA(cudaGetLastError());
+    ++g_launches;
+    return;
+  }
   // few signals -> one per thread and more row chunks; many -> 4 per thread
   const int fs = a.m >= 4LL * ctx.sm_count * kFT * 4 ? 4 : 1;
   const int64_t per_cta = (int64_t)kFT * fs;

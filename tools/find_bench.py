@@ -36,7 +36,8 @@ def main():
         sig = torch.from_numpy(rng.random((args.m, 3))).cuda()
         idx = torch.empty((args.m, 2), dtype=torch.int64, device="cuda")
         d2 = torch.empty((args.m, 2), dtype=torch.float64, device="cuda")
-        st = torch.cuda.current_stream()
+        torch.cuda.synchronize()
+        st = torch.cuda.Stream()  # a real stream: handle 0 would mean the context's own stream
 
         def run():
             _lib.check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(), args.m,
@@ -46,7 +47,8 @@ def main():
         torch.cuda.synchronize()
         times = []
         for _ in range(args.reps):
-            flush.zero_()
+            with torch.cuda.stream(st):
+                flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             run()
