@@ -311,14 +311,15 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-        fb = C.c_int64()
-        _lib_check(lib.gs_find_last_fallbacks(ctx.handle, C.byref(fb)))
+        fb2 = np.zeros(2, np.int64)
+        _lib_check(lib.gs_find_last_fallback_counts(ctx.handle, fb2))
         ms = statistics.median(times)
         pairs = float(n) * m
         achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
         out["lines"].append({"n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),
                              "achieved_tflops": achieved, "peak_tflops": peak,
-                             "frac": achieved / peak, "fallback_signals": fb.value})
+                             "frac": achieved / peak, "fallback_signals": int(fb2[0]),
+                             "fp64_rescans": int(fb2[1])})
         del pos, sig, idx, d2
     out["peak_source"] = (f"nominal FP32 2x128 lanes x {ctx.sm_count} SMs at the sampled "
                           f"{sm_mhz:.0f} MHz; 8 FLOP per pair (BASELINE.md 2)")

@@ -92,8 +92,12 @@ typedef enum {
  * certify and re-scanned exactly. */
 gs_status gs_find_device(gs_ctx *ctx, const double *d_pos, int64_t n, const double *d_sig,
                          int64_t m, int64_t *d_idx, double *d_d2, int mode, void *stream);
-/* Signals re-scanned exactly by the last GS_FIND_FILTER call on this ctx (syncs). */
+/* Signals the last GS_FIND_FILTER call on this ctx could not certify and
+ * re-scanned (syncs). */
 gs_status gs_find_last_fallbacks(gs_ctx *ctx, int64_t *count);
+/* out[0]: signals re-scanned by the FP32 direct-form tier; out[1]: of those,
+ * signals that also needed the exact FP64 scan (syncs). */
+gs_status gs_find_last_fallback_counts(gs_ctx *ctx, int64_t out[2]);
 
 /* ------------------------------------------------------------------ */
 /* device-resident multi-signal engine                                  */

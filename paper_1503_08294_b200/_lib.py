@@ -60,6 +60,7 @@ _SIGNATURES = {
                                         _i64p, C.c_int64, _f64p, C.c_int64, C.c_int64]),
     "gs_find_device": (C.c_int, [_vp, _vp, C.c_int64, _vp, C.c_int64, _vp, _vp, C.c_int, _vp]),
     "gs_find_last_fallbacks": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "gs_find_last_fallback_counts": (C.c_int, [_vp, _i64p]),
     "gs_engine_create": (C.c_int, [_vp, C.POINTER(GsParams), C.c_int64, C.POINTER(_vp)]),
     "gs_engine_destroy": (None, [_vp]),
     "gs_engine_add_unit": (C.c_int, [_vp, C.c_double, C.c_double, C.c_double, C.c_double,

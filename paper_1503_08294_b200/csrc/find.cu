@@ -361,13 +361,21 @@ extern "C" gs_status gs_find_device(gs_ctx* ctx, const double* d_pos, int64_t n,
 }
 
 extern "C" gs_status gs_find_last_fallbacks(gs_ctx* ctx, int64_t* count) {
+  int64_t both[2];
+  const gs_status st = gs_find_last_fallback_counts(ctx, both);
+  if (st == GS_OK && count) *count = both[0];
+  return st;
+}
+
+extern "C" gs_status gs_find_last_fallback_counts(gs_ctx* ctx, int64_t out[2]) {
   return guarded([&] {
-    GS_CHECK(ctx && count, GS_VALUE_ERROR, "null argument");
-    unsigned long long v = 0;
+    GS_CHECK(ctx && out, GS_VALUE_ERROR, "null argument");
+    unsigned v[2] = {0u, 0u};
     if (ctx->d_fallbacks) {
       GS_CUDA(cudaDeviceSynchronize());
-      GS_CUDA(cudaMemcpy(&v, ctx->d_fallbacks, sizeof(v), cudaMemcpyDeviceToHost));
+      GS_CUDA(cudaMemcpy(v, ctx->d_fallbacks, sizeof(v), cudaMemcpyDeviceToHost));
     }
-    *count = (int64_t)v;
+    out[0] = (int64_t)v[0];
+    out[1] = (int64_t)v[1];
   });
 }

@@ -55,13 +55,13 @@ def main():
             e1.record(st)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
-        fb = C.c_int64()
-        _lib.check(lib.gs_find_last_fallbacks(ctx.handle, C.byref(fb)))
+        fb2 = np.zeros(2, np.int64)
+        _lib.check(lib.gs_find_last_fallback_counts(ctx.handle, fb2))
         ms = sorted(times)[len(times) // 2]
         pairs = float(n) * args.m
         print(json.dumps({"n": n, "m": args.m, "mode": args.mode, "ms": ms,
                           "pairs_per_s": pairs / (ms * 1e-3), "tflops_8": 8 * pairs / (ms * 1e-3) / 1e12,
-                          "fallbacks": fb.value, "times": times}), flush=True)
+                          "fallbacks": int(fb2[0]), "fp64_rescans": int(fb2[1]), "times": times}), flush=True)
 
 
 if __name__ == "__main__":
