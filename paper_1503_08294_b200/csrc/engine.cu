@@ -58,7 +58,10 @@ constexpr int kMaxDeg = 64;  // adjacency slots per unit (overflow -> loud error
 constexpr int32_t kNone32 = 0x7f7f7f7f;
 constexpr long long kNone64 = 0x7f7f7f7f7f7f7f7fLL;
 constexpr int kRingDisk = 0, kRingHalf = 1, kRingInc = 2;
-constexpr int kUpdThreads = 1024;
+#ifndef GS_UPD_THREADS
+#define GS_UPD_THREADS 512
+#endif
+constexpr int kUpdThreads = GS_UPD_THREADS;
 constexpr long long kSweepEvery = 1024;  // engine.py:98
 constexpr int kAffCap = kMaxDeg * (kMaxDeg + 2) + 64;
 constexpr int kDeferCap = 16384;
@@ -95,6 +98,8 @@ struct Counters {
   int converged;
   int nwalk, defer_n, ev_fired, ev_b;
   long long ev_cutoff;
+  long long prof_max[4];  // GS_PROF: per-window max thread cycles (B, walk, C1, A)
+  long long prof_lv[5], prof_lvsum[5];
 };
 
 struct Params {

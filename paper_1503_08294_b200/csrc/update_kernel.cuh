@@ -25,40 +25,109 @@
 //      sweep's stale scan is block-parallel); the next window starts after it.
 
 
+// Neighbour lists up to kStage long are staged in registers so their loads
+// (and the loads that depend on them) issue together instead of as a chain
+// of dependent L2 round trips; longer lists take the plain loops.
+#ifndef GS_STAGE
+#define GS_STAGE 8
+#endif
+constexpr int kStage = GS_STAGE;
+
+// 16-byte loads: two entries per load, so a row costs half the LSU
+// wavefronts (these scattered loads are what bounds the window phases)
+__device__ __forceinline__ void stage_adj(const int2* A, int d, int2 (&nb)[kStage]) {
+  const int4* A4 = reinterpret_cast<const int4*>(A);
+#pragma unroll
+  for (int k = 0; k < kStage / 2; ++k) {
+    const int4 v = 2 * k < d ? A4[k] : make_int4(-1, -1, -1, -1);
+    nb[2 * k] = make_int2(v.x, v.y);
+    nb[2 * k + 1] = 2 * k + 1 < d ? make_int2(v.z, v.w) : make_int2(-1, -1);
+  }
+}
+
+__device__ __forceinline__ void replay_event(double4& p, double& h, const Params& P,
+                                             const double* sig, int key) {
+  const size_t j = (size_t)(key >> 1);
+  const double x = sig[3 * j], y = sig[3 * j + 1], z = sig[3 * j + 2];
+  if (key & 1) {
+    move_toward(p, P.eps_b, x, y, z);
+    h = dmul(h, P.c_b);
+  } else {
+    move_toward(p, P.eps_n, x, y, z);
+    h = dmul(h, P.c_n);
+  }
+}
+
 // replay unit u's updates from the committed signals (< jstar) of this window
+// in batch order: keys (j << 1) | self are unique (a signal has one winner),
+// so "smallest key above the last one" walks them in order without sorting.
 __device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
                           int jstar) {
   const int2* A = S.adj + (size_t)u * kMaxDeg;
   const int d = S.deg[u];
-  int t[kMaxDeg + 1];  // (j << 1) | self
-  int n = 0;
   const int jself = S.firstwin[u];
-  if (jself < jstar) t[n++] = (jself << 1) | 1;
-  for (int k = 0; k < d; ++k) {
-    const int jw = S.firstwin[A[k].x];
-    if (jw < jstar) t[n++] = jw << 1;
-  }
-  for (int i = 1; i < n; ++i) {  // insertion sort: n is a handful
-    const int x = t[i];
-    int q = i - 1;
-    while (q >= 0 && t[q] > x) {
-      t[q + 1] = t[q];
-      --q;
-    }
-    t[q + 1] = x;
-  }
   double4 p = S.pos[u];
   const double h0 = S.hab[u];
   double h = h0;
-  for (int i = 0; i < n; ++i) {
-    const size_t j = (size_t)(t[i] >> 1);
-    const double x = sig[3 * j], y = sig[3 * j + 1], z = sig[3 * j + 2];
-    if (t[i] & 1) {
-      move_toward(p, P.eps_b, x, y, z);
-      h = dmul(h, P.c_b);
-    } else {
-      move_toward(p, P.eps_n, x, y, z);
-      h = dmul(h, P.c_n);
+  constexpr int kNone = 0x7fffffff;
+  if (d <= kStage) {
+    int2 nb[kStage];
+    stage_adj(A, d, nb);
+    int key[kStage + 1];
+#pragma unroll
+    for (int k = 0; k < kStage; ++k) {
+      const int jw = k < d ? S.firstwin[nb[k].x] : kNone;
+      key[k] = jw < jstar ? (jw << 1) : kNone;
+    }
+    key[kStage] = jself < jstar ? ((jself << 1) | 1) : kNone;
+    // four events per group: their signal loads issue together
+    int last = -1;
+#pragma unroll 1
+    for (int grp = 0; grp < (kStage + 4) / 4; ++grp) {
+      int cur[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int c = kNone;
+#pragma unroll
+        for (int k = 0; k <= kStage; ++k) c = (key[k] > last && key[k] < c) ? key[k] : c;
+        cur[q] = c;
+        if (c != kNone) last = c;
+      }
+      double xs[4], ys[4], zs[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (cur[q] != kNone) {
+          const size_t j = (size_t)(cur[q] >> 1);
+          xs[q] = sig[3 * j];
+          ys[q] = sig[3 * j + 1];
+          zs[q] = sig[3 * j + 2];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (cur[q] == kNone) break;
+        if (cur[q] & 1) {
+          move_toward(p, P.eps_b, xs[q], ys[q], zs[q]);
+          h = dmul(h, P.c_b);
+        } else {
+          move_toward(p, P.eps_n, xs[q], ys[q], zs[q]);
+          h = dmul(h, P.c_n);
+        }
+      }
+      if (cur[3] == kNone) break;
+    }
+  } else {
+    int last = -1;
+    while (true) {
+      int cur = (jself < jstar && ((jself << 1) | 1) > last) ? ((jself << 1) | 1) : kNone;
+      for (int k = 0; k < d; ++k) {
+        const int jw = S.firstwin[A[k].x];
+        const int kk = jw < jstar ? (jw << 1) : kNone;
+        if (kk > last && kk < cur) cur = kk;
+      }
+      if (cur == kNone) break;
+      replay_event(p, h, P, sig, cur);
+      last = cur;
     }
   }
   S.pos[u] = p;
@@ -186,7 +255,34 @@ __device__ int event_part1b(const DevState& S, const Params& P, int b, int s, do
 // cross-CTA values travel through distributed shared memory and every
 // exchange is fenced by the hardware cluster barrier.
 
-constexpr int kCluster = 8;
+#ifndef GS_CLUSTER
+#define GS_CLUSTER 8
+#endif
+constexpr int kCluster = GS_CLUSTER;
+
+// cluster-wide barrier (a plain block barrier for a one-CTA "cluster")
+__device__ __forceinline__ void csync() {
+  if constexpr (kCluster == 1) {
+    __syncthreads();
+  } else {
+    cg::this_cluster().sync();
+  }
+}
+template <class T>
+__device__ __forceinline__ T* cmap(T* p, int rank) {
+  if constexpr (kCluster == 1) {
+    return p;
+  } else {
+    return cg::this_cluster().map_shared_rank(p, rank);
+  }
+}
+__device__ __forceinline__ int crank_of() {
+  if constexpr (kCluster == 1) {
+    return 0;
+  } else {
+    return (int)cg::this_cluster().block_rank();
+  }
+}
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
 constexpr int kWalkCap = 6 * kUpdThreads;      // per-CTA replay queue (overflow: global)
 
@@ -200,15 +296,14 @@ __device__ __forceinline__ void push_walk(const DevState& S, int* s_walk, int* s
 // used with alternating parity so a CTA running one call ahead cannot
 // overwrite values another CTA has not read yet.
 __device__ int cl_excl_scan(int v, int* s_warp, int (*s_cta)[kCluster], int& parity, int* total) {
-  cg::cluster_group cl = cg::this_cluster();
   int btot;
   const int r = block_excl_scan(v, s_warp, &btot);
-  const int me = (int)cl.block_rank();
+  const int me = crank_of();
   if (threadIdx.x < kCluster) {
-    int* dst = cl.map_shared_rank(&s_cta[parity][0], threadIdx.x);
+    int* dst = cmap(&s_cta[parity][0], threadIdx.x);
     dst[me] = btot;
   }
-  cl.sync();
+  csync();
   int off = 0, tot = 0;
 #pragma unroll
   for (int q = 0; q < kCluster; ++q) {
@@ -222,14 +317,13 @@ __device__ int cl_excl_scan(int v, int* s_warp, int (*s_cta)[kCluster], int& par
 }
 
 __device__ int cl_min(int v, int* s_warp, int (*s_cta)[kCluster], int& parity) {
-  cg::cluster_group cl = cg::this_cluster();
   const int bmin = block_min(v, s_warp);
-  const int me = (int)cl.block_rank();
+  const int me = crank_of();
   if (threadIdx.x < kCluster) {
-    int* dst = cl.map_shared_rank(&s_cta[parity][0], threadIdx.x);
+    int* dst = cmap(&s_cta[parity][0], threadIdx.x);
     dst[me] = bmin;
   }
-  cl.sync();
+  csync();
   int x = 0x7fffffff;
 #pragma unroll
   for (int q = 0; q < kCluster; ++q) x = min(x, s_cta[parity][q]);
@@ -239,14 +333,13 @@ __device__ int cl_min(int v, int* s_warp, int (*s_cta)[kCluster], int& parity) {
 
 __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_ctal)[kCluster],
                                int& parity) {
-  cg::cluster_group cl = cg::this_cluster();
   const long long bmin = block_min_ll(v, s_ll32);
-  const int me = (int)cl.block_rank();
+  const int me = crank_of();
   if (threadIdx.x < kCluster) {
-    long long* dst = cl.map_shared_rank(&s_ctal[parity][0], threadIdx.x);
+    long long* dst = cmap(&s_ctal[parity][0], threadIdx.x);
     dst[me] = bmin;
   }
-  cl.sync();
+  csync();
   long long x = 0x7fffffffffffffffLL;
 #pragma unroll
   for (int q = 0; q < kCluster; ++q) x = s_ctal[parity][q] < x ? s_ctal[parity][q] : x;
@@ -257,10 +350,14 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 // ---------------------------------------------------------------------------
 // the batch update kernel: one cluster of kCluster CTAs (8 SMs)
 
-__global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 1)
+#if GS_CLUSTER > 1
+#define GS_CLUSTER_DIMS __cluster_dims__(kCluster, 1, 1)
+#else
+#define GS_CLUSTER_DIMS
+#endif
+__global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     k_update_batch(DevState S, Params P, const double* __restrict__ sig,
                    const WinRec* __restrict__ rec, int m, int batch_no) {
-  cg::cluster_group cl = cg::this_cluster();
   __shared__ int s_warp[33];
   __shared__ long long s_ll32[33];
   __shared__ int s_cta[2][kCluster];
@@ -276,7 +373,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
   __shared__ int s_defer_n;
   Counters* c = S.cnt;
   const int tid = threadIdx.x;
-  const int crank = (int)cl.block_rank();
+  const int crank = crank_of();
   const int g = crank * kUpdThreads + tid;  // cluster-wide thread index
   const bool lead = crank == 0 && tid == 0;
   const int warp = tid >> 5, lane = tid & 31;
@@ -291,7 +388,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
     c->nwalk = 0;
   }
   if (tid == 0) s_nwalk = 0;
-  cl.sync();
+  csync();
   int j0 = 0;
   while (j0 < m) {
     if (lead) t_ph = clock64();
@@ -326,19 +423,26 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
     int nproc;
     const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
     if (proc) {
-      int* dst = cl.map_shared_rank(s_plist, rank / kUpdThreads);
+      int* dst = cmap(s_plist, rank / kUpdThreads);
       dst[rank % kUpdThreads] = j;
     }
-    cl.sync();
+    csync();
     if (lead) { const long long t_ = clock64(); c->cyc_phase[1] += t_ - t_ph; t_ph = t_; }
     // ---- B: events and adapt_threshold outcomes; thread g owns rank g
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     int evr = 0x7fffffff;
+#ifdef GS_PROF
+    const long long tb0 = clock64();
+#define GS_TS(var, dep) long long var; asm volatile("mov.u64 %0, %%clock64;" : "=l"(var) : "r"((int)(dep)) : "memory")
+#endif
     if (g < nproc) {
       const int r = g;
       const int jj = s_plist[tid];
       const WinRec w = rec[jj];
       const int b = w.b, s = w.s;
+#ifdef GS_PROF
+      GS_TS(t1, b);
+#endif
       const long long tick_j = tick0 + r + 1;
       bool ev = iso;
       if (tick_j >= next_sweep && ((tick_j - next_sweep) % kSweepEvery) == 0) {
@@ -350,28 +454,82 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
       // habituation only decays, so a unit trained at the window start stays
       // trained: exact per-time values are replayed only for untrained units
       const double hbT = S.hab[b];
+      const double thb = S.theta[b];
+      const long long la_b = S.la_val[b], la_s = S.la_val[s];
       const bool b_trained = hbT < P.h_t;
       bool found = false;
       int kcn = 0;
-      for (int k = 0; k < db; ++k) {
-        const int2 ent = B[k];
-        const int v = ent.x;
-        const bool is_s = v == s;
-        found |= is_s;
-        const int age = is_s ? 0 : S.eage[ent.y];
-        const bool age_risk = !is_s && age + 2 > P.max_age;
-        if (!b_trained || age_risk) {
-          const int jv = S.firstwin[v];
-          if (jv < jj) kcn++;
-          if (age_risk) {
-            const int a2 = jv < jj ? ((rec[jv].s == b) ? 0 : age + 1) : age;
-            if (a2 + 1 > P.max_age) ev = true;
+#ifdef GS_PROF
+      GS_TS(t2, db + (int)la_b + (int)thb + (int)hbT);
+      long long t3 = t2, t4 = t2, t5 = t2;
+#endif
+      if (db <= kStage) {
+        int2 nb[kStage];
+        stage_adj(B, db, nb);
+#ifdef GS_PROF
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t3) : "r"(nb[0].x + nb[db > 1 ? 1 : 0].y) : "memory");
+#endif
+        int age[kStage], jv[kStage];
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          const bool valid = k < db, is_s = nb[k].x == s;
+          found |= valid && is_s;
+          age[k] = (valid && !is_s) ? S.eage[nb[k].y] : 0;
+          jv[k] = valid ? S.firstwin[nb[k].x] : kNone32;
+        }
+#ifdef GS_PROF
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t4) : "r"(jv[0] + age[0] + jv[db > 1 ? 1 : 0]) : "memory");
+#endif
+        int sv[kStage];
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          const bool risk = k < db && nb[k].x != s && age[k] + 2 > P.max_age;
+          sv[k] = (risk && jv[k] < jj) ? rec[jv[k]].s : -1;
+        }
+#ifdef GS_PROF
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t5) : "r"(sv[0] + sv[1]) : "memory");
+#endif
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          if (k >= db) continue;
+          const bool age_risk = nb[k].x != s && age[k] + 2 > P.max_age;
+          if (!b_trained || age_risk) {
+            if (jv[k] < jj) kcn++;
+            if (age_risk) {
+              const int a2 = jv[k] < jj ? ((sv[k] == b) ? 0 : age[k] + 1) : age[k];
+              if (a2 + 1 > P.max_age) ev = true;
+            }
+          }
+        }
+      } else {
+        for (int k = 0; k < db; ++k) {
+          const int2 ent = B[k];
+          const int v = ent.x;
+          const bool is_s = v == s;
+          found |= is_s;
+          const int age = is_s ? 0 : S.eage[ent.y];
+          const bool age_risk = !is_s && age + 2 > P.max_age;
+          if (!b_trained || age_risk) {
+            const int jv = S.firstwin[v];
+            if (jv < jj) kcn++;
+            if (age_risk) {
+              const int a2 = jv < jj ? ((rec[jv].s == b) ? 0 : age + 1) : age;
+              if (a2 + 1 > P.max_age) ev = true;
+            }
           }
         }
       }
       if (!found) ev = true;  // connect_or_reset creates b-s
       const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, kcn), P.c_b) < P.h_t;
-      if (hb_low && w.dwin > S.theta[b]) ev = true;  // maybe_insert fires
+      if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
+#ifdef GS_PROF
+      atomicMax(&c->prof_max[2], clock64() - tb0);
+      atomicMax(&c->prof_lv[0], t1 - tb0);
+      atomicMax(&c->prof_lv[1], t2 - t1);
+      atomicMax(&c->prof_lv[2], t3 - t2);
+      atomicMax(&c->prof_lv[3], t4 - t3);
+      atomicMax(&c->prof_lv[4], t5 - t4);
+#endif
       int pat = -2;
       if (!ev) {
         const int ring = S.ring[b];
@@ -410,12 +568,15 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
       }
       s_pat[tid] = pat;
       // last_active presence at the window start (dict order stamps)
-      s_abs[tid] = (unsigned char)((S.la_val[b] == -1 ? 1 : 0) | (S.la_val[s] == -1 ? 2 : 0));
+      s_abs[tid] = (unsigned char)((la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0));
       if (ev) evr = r;
     }
+#ifdef GS_PROF
+    if (g < nproc) atomicMax(&c->prof_max[0], clock64() - tb0);
+#endif
     const int rstar = min(cl_min(evr, s_warp, s_cta, parity), nproc);
     if (tid == 0) {
-      s_i[4] = rstar < nproc ? cl.map_shared_rank(s_plist, rstar / kUpdThreads)[rstar % kUpdThreads]
+      s_i[4] = rstar < nproc ? cmap(s_plist, rstar / kUpdThreads)[rstar % kUpdThreads]
                              : wend;
     }
     __syncthreads();
@@ -446,26 +607,62 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
       if (atomicExch(&S.touchfirst[cw.b], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, cw.b);
       const int db = S.deg[cw.b];
       const int2* B = S.adj + (size_t)cw.b * kMaxDeg;
-      for (int k = 0; k < db; ++k) {
-        const int2 ent = B[k];
-        const int v = ent.x;
-        if (atomicExch(&S.touchfirst[v], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, v);
-        const int jv = S.firstwin[v];
-        if (jv < jstar && jv > cj) continue;  // v's own signal replays this edge
-        int age = S.eage[ent.y];
-        if (jv < cj) age = (rec[jv].s == cw.b) ? 0 : age + 1;
-        age = (v == cw.s) ? 0 : age + 1;
-        S.eage[ent.y] = age;
+      if (db <= kStage) {
+        int2 nb[kStage];
+        stage_adj(B, db, nb);
+        int tf[kStage], jv[kStage], age[kStage];
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          if (k < db) {
+            tf[k] = atomicExch(&S.touchfirst[nb[k].x], 1);
+            jv[k] = S.firstwin[nb[k].x];
+            age[k] = S.eage[nb[k].y];
+          }
+        }
+        int sv[kStage];
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          const bool mine = k < db && !(jv[k] < jstar && jv[k] > cj);
+          sv[k] = (mine && jv[k] < cj) ? rec[jv[k]].s : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          if (k >= db) continue;
+          if (tf[k] == kNone32) push_walk(S, s_walk, &s_nwalk, nb[k].x);
+          if (jv[k] < jstar && jv[k] > cj) continue;  // v's own signal replays this edge
+          int a = age[k];
+          if (jv[k] < cj) a = (sv[k] == cw.b) ? 0 : a + 1;
+          a = (nb[k].x == cw.s) ? 0 : a + 1;
+          S.eage[nb[k].y] = a;
+        }
+      } else {
+        for (int k = 0; k < db; ++k) {
+          const int2 ent = B[k];
+          const int v = ent.x;
+          if (atomicExch(&S.touchfirst[v], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, v);
+          const int jv = S.firstwin[v];
+          if (jv < jstar && jv > cj) continue;  // v's own signal replays this edge
+          int age = S.eage[ent.y];
+          if (jv < cj) age = (rec[jv].s == cw.b) ? 0 : age + 1;
+          age = (v == cw.s) ? 0 : age + 1;
+          S.eage[ent.y] = age;
+        }
       }
     }
-    cl.sync();
+    csync();
     if (lead) { const long long t_ = clock64(); c->cyc_phase[3] += t_ - t_ph; t_ph = t_; }
     // ---- C2: each touched unit's position / habituation sequence replayed once
     const int nloc = min(s_nwalk, kWalkCap);
+#ifdef GS_PROF
+    const long long tw0 = clock64();
+#endif
     for (int i = tid; i < nloc; i += kUpdThreads) walk_unit(S, P, sig, s_walk[i], jstar);
+#ifdef GS_PROF
+    if (tid < nloc) atomicMax(&c->prof_max[1], clock64() - tw0);
+#endif
     const int nglob = c->nwalk;  // overflow list (only for very high degrees)
     for (int i = g; i < nglob; i += kWinC) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
-    cl.sync();
+    csync();
     if (lead) { const long long t_ = clock64(); c->cyc_phase[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
     if (lead) {
@@ -480,12 +677,22 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
     if (cand) S.firstwin[cb] = kNone32;
     for (int i = tid; i < nloc; i += kUpdThreads) S.touchfirst[s_walk[i]] = kNone32;
     for (int i = g; i < nglob; i += kWinC) S.touchfirst[(int)S.scratch[i]] = kNone32;
-    cl.sync();
+    csync();
     if (tid == 0) s_nwalk = 0;
     if (lead) {
       c->nwalk = 0;
       const long long t_ = clock64();
       c->cyc_phase[7] += t_ - t_ph;
+#ifdef GS_PROF
+      c->cyc_phase[4] += c->prof_max[0];
+      c->cyc_phase[5] += c->prof_max[1];
+      c->prof_max[3] += c->prof_max[2];
+      c->prof_max[0] = c->prof_max[1] = c->prof_max[2] = 0;
+      for (int q = 0; q < 5; ++q) {
+        c->prof_lvsum[q] += c->prof_lv[q];
+        c->prof_lv[q] = 0;
+      }
+#endif
       t_ph = t_;
     }
     // ---- D: the event signal, exactly as update_single (CTA 0)
@@ -539,7 +746,7 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
           c->defer_n = s_defer_n;
         }
       }
-      cl.sync();
+      csync();
       // deferred ring reclassification, one warp per affected unit (cluster-wide)
       {
         const int nd = min(c->defer_n, kDeferCap);
@@ -572,12 +779,12 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
           }
         }
       }
-      cl.sync();
+      csync();
       if (lead) {
         serial_update_part2(S, P, c->ev_b, c->stale_n, fired != 0);
         c->cyc_serial += clock64() - t_ser;
       }
-      cl.sync();
+      csync();
       j0 = jstar + 1;
     } else {
       j0 = wend;
@@ -629,5 +836,13 @@ __global__ void __cluster_dims__(kCluster, 1, 1) __launch_bounds__(kUpdThreads, 
     st->cyc_serial = c->cyc_serial;
     st->cyc_total = c->cyc_total;
     for (int q = 0; q < 8; ++q) st->cyc_phase[q] = c->cyc_phase[q];
+#ifdef GS_PROF
+    st->cyc_phase[1] = c->prof_max[3];  // profiling builds: B event-detection max replaces "scan"
+    st->ev_create = c->prof_lvsum[0];
+    st->ev_insert = c->prof_lvsum[1];
+    st->ev_prune = c->prof_lvsum[2];
+    st->ev_sweep = c->prof_lvsum[3];
+    st->cyc_serial = c->prof_lvsum[4];
+#endif
   }
 }

@@ -35,4 +35,4 @@ print(f"{name}: batches={b+1} signals={signals} V={units} conv={bool(st.converge
       f"insert={st.ev_insert} prune={st.ev_prune} sweep={st.ev_sweep} "
       f"serial-cycles={st.cyc_serial/max(1,st.cyc_total):.3f} of {st.cyc_total/1.9e9:.3f}s", flush=True)
 print("  window phases (s): " + " ".join(f"{n}={st.cyc_phase[i]/1.9e9:.3f}" for i, n in enumerate(
-    ("A+minla", "scan", "B", "C1", "C2", "C3?", "walk", "cnt+reset"))))
+    ("A+minla", "scan|Bdetect-max", "B", "C1", "Bmax", "walkmax", "walk", "cnt+reset"))))
