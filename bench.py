@@ -52,6 +52,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
     p.add_argument("--no-find-microbench", action="store_true")
+    p.add_argument("--no-m-sweep", action="store_true")
     return p.parse_args()
 
 
@@ -317,6 +318,8 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
         pairs = float(n) * m
         achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
         out["lines"].append({"n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),
+                             "algorithmic_bytes": 24 * n + 56 * m,
+                             "traffic": ncu_traffic({1_000_000: "filter", 100_000: "filter_n1e5"}.get(n, "")),
                              "achieved_tflops": achieved, "peak_tflops": peak,
                              "frac": achieved / peak, "fallback_signals": int(fb2[0]),
                              "fp64_rescans": int(fb2[1])})
@@ -349,6 +352,59 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
     return out
 
 
+def m_sweep(lib, src, wparams, seed, ms=(256, 1024, 4096, 16384, 65536), budget_s=20.0):
+    """BASELINE config 3's m sweep: the same seeded run at each fixed batch
+    size, device sampling + asynchronous loop, timed with CUDA events on the
+    engine stream; a run that has not converged after budget_s seconds of
+    device time (or the signal cap) is reported as such."""
+    import numpy as np
+    import torch
+
+    from paper_1503_08294_b200 import EngineParams, _lib
+    from paper_1503_08294_b200.device_sampling import DeviceCloudSampler
+    from paper_1503_08294_b200.network import Network
+
+    out = []
+    pts_dev = torch.from_numpy(src.points).cuda()
+    for m in ms:
+        p = dict(wparams)
+        p.update(batch_floor=m, batch_cap=m)
+        params = EngineParams(**p)
+        rng = np.random.Generator(np.random.Philox(seed))
+        seeds = src.sample(rng, 2)
+        net = Network(params, capacity=8192)
+        net.reserve(8192)
+        net.set_async(8)
+        sampler = DeviceCloudSampler(None, rng, device_ptr=pts_dev.data_ptr(),
+                                     npts=src.points.shape[0])
+        for s_ in seeds:
+            net.add_unit(s_, params.theta0)
+        stream = torch.cuda.ExternalStream(net.stream_handle())
+        st = _lib.GsBatchStats()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        enq = 0
+        while enq * m < params.max_signals:
+            _lib_check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
+            enq += 1
+            if enq % 8 == 0:
+                _lib_check(lib.gs_engine_stats(net.handle, C.byref(st)))
+                if st.converged or time.perf_counter() - t0 > budget_s:
+                    break
+        e1.record(stream)
+        _lib_check(lib.gs_engine_stats(net.handle, C.byref(st)))
+        sec = e0.elapsed_time(e1) * 1e-3
+        sig = int(st.batches) * m
+        out.append({"m": m, "converged": bool(st.converged), "signals": sig,
+                    "batches": int(st.batches), "device_s": sec, "signals_per_s": sig / sec,
+                    "units": int(st.units), "edges": int(st.edges)})
+        sampler.close()
+        net.close()
+    return out
+
+
 def _lib_check(rc):
     from paper_1503_08294_b200 import _lib
 
@@ -372,36 +428,57 @@ def run_b200_arm(args):
     if params.batch_floor != params.batch_cap:
         raise SystemExit("bench workloads use a fixed batch size")
     m = params.batch_cap
-    # seeded stream: 2 seed units then batches; CloudSource batches concatenate
+    # inputs resident in HBM: the cloud; signals are drawn on the device from
+    # the same Philox stream as the reference (device_sampling.py)
+    from paper_1503_08294_b200.device_sampling import DeviceCloudSampler, philox_state_words
+
     rng = np.random.Generator(np.random.Philox(seed))
     seeds = src.sample(rng, 2)
-    total = -(-params.max_signals // m) * m
-    idx = src.sample_indices(rng, total)
-    stream_dev = torch.from_numpy(src.points).cuda()[torch.from_numpy(idx).cuda()].contiguous()
-    del idx
-    stream_bytes = stream_dev.numel() * 8
+    state0 = philox_state_words(rng)
+    pts_dev = torch.from_numpy(src.points).cuda()
+    cloud_bytes = pts_dev.numel() * 8
+    sampler = DeviceCloudSampler(None, device_ptr=pts_dev.data_ptr(), npts=src.points.shape[0])
+    sig_buf = torch.empty((m, 3), dtype=torch.float64, device="cuda")
     net = Network(params, capacity=8192)
     net.reserve(8192)
     sharded = ShardedStep(net) if world > 1 else None
+    if sharded is None:
+        net.set_async(8)
     engine_stream = torch.cuda.ExternalStream(net.stream_handle())
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     st = _lib.GsBatchStats()
-    base_ptr = stream_dev.data_ptr()
+    torch.cuda.synchronize()
+
+    LOOKAHEAD = 8  # batches enqueued ahead of the convergence check
 
     def one_run(trace=None):
         net.reset()
         for s in seeds:
             net.add_unit(s, params.theta0)
+        _lib.check(lib.gs_sampler_set_state(sampler.handle, state0))
+        if trace is None and sharded is None:
+            # device-resident loop: the host only polls the convergence flag;
+            # batches after convergence are no-ops on the device (halted)
+            enq = 0
+            while enq * m < params.max_signals:
+                _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
+                enq += 1
+                if enq % LOOKAHEAD == 0:
+                    _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
+                    if st.converged:
+                        break
+            _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
+            return int(st.batches) * m, bool(st.converged), int(st.units), int(st.edges)
         off = 0
         units = 2
         while off < params.max_signals:
-            ptr = base_ptr + off * 24
             if trace is not None:
                 trace["pairs"] += m * units
             if sharded is None:
-                _lib.check(lib.gs_engine_step_device(net.handle, ptr, m))
+                _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
             else:
-                sharded.step_device(ptr, m)
+                sampler.draw(m, sig_buf.data_ptr(), net.stream_handle())
+                sharded.step_device(sig_buf.data_ptr(), m)
             _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
             off += m
             units = int(st.units)
@@ -501,7 +578,7 @@ def run_b200_arm(args):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_s = float(t.item())
         e2e = {"value": e_sig / e_s, "unit": "signals/s",
-               "h2d_bytes_per_step": int(24 * (e_sig // args.steps) + 48),
+               "h2d_bytes_per_step": int(cloud_bytes + 48 + 120),
                "d2h_bytes_per_step": int(C.sizeof(_lib.GsBatchStats) * (e_batches // args.steps)),
                "ms_per_step": 1e3 * e_s / args.steps}
 
@@ -514,6 +591,9 @@ def run_b200_arm(args):
                "sample": f"first {sig:,} signals ({batches} batches) of the same seeded "
                          f"{args.workload} run ({sec:.1f} s)"}
 
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_m_sweep:
+        sweep = m_sweep(lib, src, dict(workloads.WORKLOADS[args.workload]["params"]), seed)
     fmb = None
     if rank == 0 and not args.no_find_microbench:
         fmb = find_microbench(lib, _lib.default_context(),
@@ -532,8 +612,9 @@ def run_b200_arm(args):
                        "step": "one seeded run from the two seed units to convergence",
                        "signals_per_step": sig, "converged": conv, "units": units,
                        "edges": edges, "time_to_converge_s": ms / args.steps * 1e-3,
-                       "l2": f"256 MiB L2 flush before each step; signal stream "
-                             f"{stream_bytes / 2**20:.0f} MiB > L2",
+                       "l2": "256 MiB L2 flush before each step (cloud "
+                             f"{cloud_bytes / 2**20:.0f} MiB resident in HBM)",
+                       "sampling": "device Philox4x64-10 + Lemire, bit-identical to numpy",
                        "find_mode": "auto"},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -542,6 +623,7 @@ def run_b200_arm(args):
             "clocks": clk,
             "phase_ms_per_step": {"find": find_ms, "update": update_ms},
             "find_microbench": fmb,
+            "m_sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -124,6 +124,8 @@ typedef struct {
   int64_t ev_create, ev_insert, ev_prune, ev_sweep; /* serial-path causes (cumulative) */
   int64_t cyc_serial, cyc_total;          /* update-kernel SM cycles: serial path / all (cumulative) */
   int64_t cyc_phase[8];                   /* window phases A, scan, B, C1, C2, C3, walk, reset */
+  int64_t batches;                        /* update kernels run so far (cumulative) */
+  int64_t halted;                         /* 1: converged, later batches are no-ops (async runs) */
 } gs_batch_stats;
 
 typedef struct gs_engine gs_engine;
@@ -182,6 +184,10 @@ gs_status gs_engine_set_params(gs_engine *eng, const gs_params *params);
 gs_status gs_engine_stats(gs_engine *eng, gs_batch_stats *out);
 /* The engine's CUDA stream (cudaStream_t) for callers sharing it. */
 void *gs_engine_stream(gs_engine *eng);
+/* Allow up to `depth` batches to be enqueued ahead of the host's stats reads:
+ * once converged, later batches leave the network untouched (stats.halted),
+ * and stats.batches counts the batches that ran.  0 = synchronous contract. */
+gs_status gs_engine_set_async(gs_engine *eng, int depth);
 /* Pre-size device storage for ids [0, n) (avoids growth inside timed loops). */
 gs_status gs_engine_reserve(gs_engine *eng, int64_t n);
 /* Empty the network in place, keeping device allocations (a fresh
@@ -203,6 +209,33 @@ gs_status gs_engine_export_edges(gs_engine *eng, int64_t cap, int64_t *abage, in
 /* Device audit (Network.audit, network.py:485-526): recomputes rings, degree
  * symmetry, counters; returns the number of violations found. */
 gs_status gs_engine_audit(gs_engine *eng, int64_t *violations);
+
+/* ------------------------------------------------------------------ */
+/* device-side CloudSource sampler (sampling.py:175-177)               */
+
+/* CloudSource.sample(rng, m) == points[rng.integers(0, N, size=m)] with
+ * rng = Generator(Philox(seed)); the generator state lives on the device and
+ * every draw is bit-identical to numpy's (Philox4x64-10, Lemire bounded
+ * 32-bit draws).  points: N x 3 float64, host (copied once) or device
+ * (points_on_device = 1, borrowed; must outlive the sampler), or NULL for
+ * an index-only sampler; 1 <= N < 2^32. */
+typedef struct gs_sampler gs_sampler;
+gs_status gs_sampler_create(gs_ctx *ctx, const double *points, int64_t npts, int points_on_device,
+                            gs_sampler **out);
+void gs_sampler_destroy(gs_sampler *s);
+/* numpy Philox bit_generator.state as uint64[15]: counter[4], key[2],
+ * buffer[4], buffer_pos, has_uint32, uinteger, 0, 0 */
+gs_status gs_sampler_set_state(gs_sampler *s, const uint64_t *state);
+gs_status gs_sampler_get_state(gs_sampler *s, uint64_t *state);
+/* m signals into d_out (m x 3 float64, device); asynchronous on `stream`
+ * (NULL = the context stream); advances the device state. */
+gs_status gs_sampler_draw(gs_sampler *s, int64_t m, double *d_out, void *stream);
+/* rng.integers(0, npts, size=m) into d_idx (int64, device); a sampler made
+ * with points == NULL only draws indices. */
+gs_status gs_sampler_draw_indices(gs_sampler *s, int64_t m, int64_t *d_idx, void *stream);
+/* gs_engine_step with the batch drawn on the device by `smp`; out == NULL
+ * leaves the iteration queued (read stats later with gs_engine_stats). */
+gs_status gs_engine_step_sampled(gs_engine *eng, gs_sampler *smp, int64_t m, gs_batch_stats *out);
 
 #ifdef __cplusplus
 }

@@ -41,11 +41,13 @@ class GsBatchStats(C.Structure):
     _fields_ = [(name, C.c_int64) for name in (
         "processed", "discarded", "inserted", "units", "edges", "next_id", "converged",
         "tick", "events", "windows", "error", "max_degree", "ev_create", "ev_insert",
-        "ev_prune", "ev_sweep", "cyc_serial", "cyc_total")] + [("cyc_phase", C.c_int64 * 8)]
+        "ev_prune", "ev_sweep", "cyc_serial", "cyc_total")] + [("cyc_phase", C.c_int64 * 8)] + [
+        ("batches", C.c_int64), ("halted", C.c_int64)]
 
 
 _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 
 _SIGNATURES = {
@@ -86,11 +88,19 @@ _SIGNATURES = {
     "gs_engine_reserve": (C.c_int, [_vp, C.c_int64]),
     "gs_engine_launch_count": (C.c_int64, [_vp]),
     "gs_engine_reset": (C.c_int, [_vp]),
+    "gs_engine_set_async": (C.c_int, [_vp, C.c_int]),
     "gs_engine_counts": (C.c_int, [_vp, _i64p]),
     "gs_engine_export_units": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          C.POINTER(C.c_int64)]),
     "gs_engine_export_edges": (C.c_int, [_vp, C.c_int64, _vp, C.POINTER(C.c_int64)]),
     "gs_engine_audit": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "gs_sampler_create": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.POINTER(_vp)]),
+    "gs_sampler_destroy": (None, [_vp]),
+    "gs_sampler_set_state": (C.c_int, [_vp, _u64p]),
+    "gs_sampler_get_state": (C.c_int, [_vp, _u64p]),
+    "gs_sampler_draw": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "gs_sampler_draw_indices": (C.c_int, [_vp, C.c_int64, _vp, _vp]),
+    "gs_engine_step_sampled": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(GsBatchStats)]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -171,4 +171,7 @@ struct FindArgs {
 
 void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 
+// device CloudSource sampler (sample.cu): m signals into d_out on `stream`
+void sampler_draw(gs_sampler* s, int64_t m, double* d_out, cudaStream_t stream);
+
 }  // namespace gs

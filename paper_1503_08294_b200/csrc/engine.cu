@@ -98,6 +98,8 @@ struct Counters {
   int converged;
   int nwalk, defer_n, ev_fired, ev_b;
   long long ev_cutoff;
+  int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
+  long long batches;             // update kernels that ran (not halted)
   long long prof_max[4];  // GS_PROF: per-window max thread cycles (B, walk, C1, A)
   long long prof_lv[5], prof_lvsum[5];
 };
@@ -856,6 +858,8 @@ struct gs_engine {
   double find_ms = 0.0, update_ms = 0.0;
   // host mirror of the last known counters
   int next_id = 0, n_edges = 0, n_units = 0;
+  // batches the host may enqueue ahead of its last stats read (gs_engine_set_async)
+  int async_depth = 0;
 };
 
 namespace {
@@ -953,6 +957,9 @@ void grow_edges(gs_engine* e, int new_ec) {
 }
 
 void ensure_capacity(gs_engine* e, int64_t extra_units, int64_t extra_edges) {
+  // with batches in flight the host's counters lag: leave room for them
+  extra_units *= 1 + e->async_depth;
+  extra_edges *= 1 + e->async_depth;
   const int64_t need_u = (int64_t)e->next_id + extra_units + 1;
   if (need_u > e->U) {
     int64_t nu = std::max<int64_t>(e->U, 1024);
@@ -1318,6 +1325,27 @@ extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
   });
 }
 
+// One iteration whose m signals are drawn on the device by a CloudSource
+// sampler (sample.cu) into the engine's signal buffer; out != NULL makes it
+// synchronous (stats copied out), else it stays queued on the engine stream.
+extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64_t m,
+                                            gs_batch_stats* out) {
+  return guarded([&] {
+    GS_CHECK(e && smp && m > 0, GS_VALUE_ERROR, "bad step arguments");
+    double* d_sig = (double*)e->sig_buf.get(sizeof(double) * 3 * (size_t)m);
+    sampler_draw(smp, m, d_sig, e->stream);
+    e->launches++;
+    gs_status st = gs_engine_step_device(e, d_sig, m);
+    if (st != GS_OK) throw Fail{st};
+    if (out) {
+      GS_CUDA(cudaStreamSynchronize(e->stream));
+      harvest_timing(e);
+      check_stats(e);
+      *out = *e->h_stats;
+    }
+  });
+}
+
 extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t m,
                                     gs_batch_stats* out) {
   return guarded([&] {
@@ -1402,6 +1430,23 @@ extern "C" gs_status gs_engine_reserve(gs_engine* e, int64_t n) {
 }
 
 // Empty the network in place (no reallocation): a fresh Network() + RunState().
+// Let the host enqueue up to `depth` batches ahead of its stats reads: the
+// update kernel turns into a no-op once the network has converged (the
+// device counts the batches it really ran), and capacity checks leave room
+// for the batches in flight.  depth 0 restores the synchronous contract.
+extern "C" gs_status gs_engine_set_async(gs_engine* e, int depth) {
+  return guarded([&] {
+    GS_CHECK(e && depth >= 0 && depth <= 1024, GS_VALUE_ERROR, "bad async depth");
+    e->async_depth = depth;
+    // {halt_on_converge, halted}: leaving async mode also clears the halt, so
+    // the network can be stepped further like the reference's
+    const int flags[2] = {depth > 0 ? 1 : 0, 0};
+    GS_CUDA(cudaMemcpyAsync(&e->S.cnt->halt_on_converge, flags, (depth > 0 ? 1 : 2) * sizeof(int),
+                            cudaMemcpyHostToDevice, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+  });
+}
+
 extern "C" gs_status gs_engine_reset(gs_engine* e) {
   return guarded([&] {
     GS_CHECK(e, GS_VALUE_ERROR, "null engine");
@@ -1421,6 +1466,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     Counters init{};
     init.next_sweep = kSweepEvery;
     init.efree_top = e->EC;
+    init.halt_on_converge = e->async_depth > 0 ? 1 : 0;
     GS_CUDA(cudaMemcpyAsync(S.cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, st));
     GS_CUDA(cudaMemsetAsync(S.stats, 0, sizeof(gs_batch_stats), st));
     GS_CUDA(cudaStreamSynchronize(st));

@@ -379,6 +379,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const int warp = tid >> 5, lane = tid & 31;
   const int gwarp = crank * (kUpdThreads / 32) + warp;
   int parity = 0;
+  if (S.cnt->halted) return;  // converged earlier in an asynchronous run (uniform)
   const long long t_kernel = clock64();
   long long t_ph = t_kernel;
   if (lead) {
@@ -815,6 +816,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // is_converged: engine.py:358-365 (max(h) < h_t <=> no untrained unit)
     const int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
     c->converged = (c->n_units >= 4 && ok == c->n_units && c->untrained == 0) ? 1 : 0;
+    c->batches++;
+    if (c->converged && c->halt_on_converge) c->halted = 1;
     gs_batch_stats* st = S.stats;
     st->processed = c->processed;
     st->discarded = c->discarded;
@@ -835,6 +838,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->cyc_total += clock64() - t_kernel;
     st->cyc_serial = c->cyc_serial;
     st->cyc_total = c->cyc_total;
+    st->batches = c->batches;
+    st->halted = c->halted;
     for (int q = 0; q < 8; ++q) st->cyc_phase[q] = c->cyc_phase[q];
 #ifdef GS_PROF
     st->cyc_phase[1] = c->prof_max[3];  // profiling builds: B event-detection max replaces "scan"

@@ -82,9 +82,10 @@ def run_multi_sharded(source, params, seed: int, *, group=None, capacity: int = 
     """run_multi (multi.py:134-202) with each batch's find sharded across the
     ranks of ``group``; every rank returns the identical (Network, RunStats).
 
-    Host sampling is replicated (every rank draws the same Philox stream, so
-    signals need no communication); each batch is copied to the device once
-    per rank.
+    Sampling is replicated (every rank draws the same Philox stream, so
+    signals need no communication): on the device for a CloudSource
+    (device_sampling.py; the cloud is copied once per rank), else on the host
+    with one H2D copy per batch.
     """
     import ctypes as C
     import time
@@ -104,6 +105,13 @@ def run_multi_sharded(source, params, seed: int, *, group=None, capacity: int = 
     seeds = source.sample(rng, 2)
     for k in range(2):
         net.add_unit(seeds[k], params.theta0)
+    from .sampling import CloudSource
+
+    sampler = None
+    if isinstance(source, CloudSource):
+        from .device_sampling import DeviceCloudSampler
+
+        sampler = DeviceCloudSampler(source.points, rng)
     signals = discarded = iterations = 0
     units, edges, converged = 2, 0, False
     st = _lib.GsBatchStats()
@@ -113,15 +121,19 @@ def run_multi_sharded(source, params, seed: int, *, group=None, capacity: int = 
     t_start = time.perf_counter()
     while signals < params.max_signals:
         m = batch_size(units, params.batch_cap, params.batch_floor)
-        t0 = time.perf_counter()
-        batch = np.ascontiguousarray(source.sample(rng, m), dtype=np.float64)
-        sample_s += time.perf_counter() - t0
-        if host is None or host.shape[0] < m:
-            host = torch.empty((m, 3), dtype=torch.float64).pin_memory()
+        if dev is None or dev.shape[0] < m:
             dev = torch.empty((m, 3), dtype=torch.float64, device="cuda")
-        host[:m].copy_(torch.from_numpy(batch))
-        with torch.cuda.stream(runner.stream):
-            dev[:m].copy_(host[:m], non_blocking=True)
+            if sampler is None:
+                host = torch.empty((m, 3), dtype=torch.float64).pin_memory()
+        if sampler is not None:
+            sampler.draw(m, dev.data_ptr(), net.stream_handle())
+        else:
+            t0 = time.perf_counter()
+            batch = np.ascontiguousarray(source.sample(rng, m), dtype=np.float64)
+            sample_s += time.perf_counter() - t0
+            host[:m].copy_(torch.from_numpy(batch))
+            with torch.cuda.stream(runner.stream):
+                dev[:m].copy_(host[:m], non_blocking=True)
         runner.step_device(dev.data_ptr(), m)
         _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
         net._touch()
@@ -133,6 +145,9 @@ def run_multi_sharded(source, params, seed: int, *, group=None, capacity: int = 
             converged = True
             break
     total = time.perf_counter() - t_start
+    if sampler is not None:
+        sampler.store_state(rng)
+        sampler.close()
     stats = RunStats(variant="multi-b200-sharded", dataset=getattr(source, "label", "unknown"),
                      seed=seed, iterations=iterations, signals=signals, discarded=discarded,
                      units=units, connections=edges, total_s=total, sample_s=sample_s,

@@ -131,13 +131,21 @@ def step(net: Network, batch) -> _lib.GsBatchStats:
 
 def run_multi(source, params: EngineParams, seed: int, executor=None, *,
               variant: str = "multi-b200", dataset: str | None = None,
-              find_mode: int = _lib.FIND_AUTO, capacity: int = 4096):
+              find_mode: int = _lib.FIND_AUTO, capacity: int = 4096,
+              device_sampling: bool | None = None):
     """Run the multi-signal engine to convergence or the signal cap.
 
     Same driver contract as multi.py:134-202: Philox(seed) stream, two seed
     units from the first two samples, m = batch_size(V) per batch,
     convergence checked once per batch.  Returns (Network, RunStats).
+
+    device_sampling (default: on for a CloudSource without an executor)
+    draws every batch on the GPU from the same Philox stream
+    (device_sampling.py), so the cloud crosses PCIe once per run instead of
+    every batch's signals.
     """
+    from .sampling import CloudSource
+
     lib = _lib.load_library()
     rng = np.random.Generator(np.random.Philox(seed))
     net = Network(params, capacity=capacity, find_mode=find_mode)
@@ -145,6 +153,15 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     seeds = source.sample(rng, 2)
     for k in range(2):
         net.add_unit(seeds[k], params.theta0)
+    if device_sampling is None:
+        device_sampling = executor is None and isinstance(source, CloudSource)
+    sampler = None
+    if device_sampling:
+        if executor is not None or not isinstance(source, CloudSource):
+            raise ValueError("device sampling runs the device engine on a CloudSource")
+        from .device_sampling import DeviceCloudSampler
+
+        sampler = DeviceCloudSampler(source.points, rng)
     timer = PhaseTimer()
     signals = discarded = iterations = 0
     converged = False
@@ -155,10 +172,47 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     if executor is None:
         _lib.check(lib.gs_engine_phase_ms(net.handle, 1, phase))
     st = _lib.GsBatchStats()
+    # fixed batch size + device sampling: the host enqueues batches ahead and
+    # only polls for convergence (gs_engine_set_async); the device counts
+    # the batches that really ran and halts after convergence
+    lookahead = 8 if (sampler is not None and params.batch_floor == params.batch_cap) else 0
+    if lookahead:
+        net.set_async(lookahead)
     t_start = perf()
-    while signals < params.max_signals:
+    if lookahead:
+        m = params.batch_cap
+        enq = 0
+        while enq * m < params.max_signals:
+            _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
+            enq += 1
+            if enq % lookahead == 0:
+                _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
+                if st.converged:
+                    break
+        _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
+        net.set_async(0)
+        net._touch()
+        iterations = int(st.batches)
+        signals = iterations * m
+        discarded = signals - int(st.tick)
+        units, edges = int(st.units), int(st.edges)
+        converged = bool(st.converged)
+    while not lookahead and signals < params.max_signals:
         m = batch_size(units, params.batch_cap, params.batch_floor)
         t0 = perf()
+        if sampler is not None:
+            _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, C.byref(st)))
+            t1 = t2 = t3 = perf()
+            net._touch()
+            signals += m
+            discarded += int(st.discarded)
+            iterations += 1
+            units = int(st.units)
+            edges = int(st.edges)
+            if st.converged:
+                converged = True
+                break
+            continue
         batch = np.ascontiguousarray(source.sample(rng, m), dtype=np.float64)
         t1 = perf()
         if executor is None:
@@ -184,6 +238,9 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
             converged = True
             break
     total = perf() - t_start
+    if sampler is not None:
+        sampler.store_state(rng)
+        sampler.close()
     if executor is None:
         _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
         timer.find_s = phase[0] * 1e-3

@@ -94,6 +94,10 @@ class Network:
         _lib.check(self._lib.gs_engine_reset(self._h))
         self._touch()
 
+    def set_async(self, depth: int) -> None:
+        """Allow `depth` batches in flight ahead of stats reads (gs_engine_set_async)."""
+        _lib.check(self._lib.gs_engine_set_async(self._h, int(depth)))
+
     def reserve(self, n_ids: int) -> None:
         _lib.check(self._lib.gs_engine_reserve(self._h, int(n_ids)))
 
