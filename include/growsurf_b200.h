@@ -123,7 +123,11 @@ typedef struct {
   int64_t max_degree;                     /* largest unit degree seen (capacity check) */
   int64_t ev_create, ev_insert, ev_prune, ev_sweep; /* serial-path causes (cumulative) */
   int64_t cyc_serial, cyc_total;          /* update-kernel SM cycles: serial path / all (cumulative) */
-  int64_t cyc_phase[8];                   /* window phases A, scan, B, C1, C2, C3, walk, reset */
+  int64_t cyc_phase[12];                  /* update-kernel SM cycles (cumulative): window phases
+                                           * 0 A+scan, 2 B, 3 C1, 6 walk, 7 reset; event path
+                                           * 4 connect/age+moves, 5 insert+prune, 1 ring
+                                           * reclassification, 8 adapt_threshold, 9 barrier;
+                                           * 10, 11 spare */
   int64_t batches;                        /* update kernels run so far (cumulative) */
   int64_t halted;                         /* 1: converged, later batches are no-ops (async runs) */
 } gs_batch_stats;

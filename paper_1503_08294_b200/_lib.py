@@ -41,7 +41,7 @@ class GsBatchStats(C.Structure):
     _fields_ = [(name, C.c_int64) for name in (
         "processed", "discarded", "inserted", "units", "edges", "next_id", "converged",
         "tick", "events", "windows", "error", "max_degree", "ev_create", "ev_insert",
-        "ev_prune", "ev_sweep", "cyc_serial", "cyc_total")] + [("cyc_phase", C.c_int64 * 8)] + [
+        "ev_prune", "ev_sweep", "cyc_serial", "cyc_total")] + [("cyc_phase", C.c_int64 * 12)] + [
         ("batches", C.c_int64), ("halted", C.c_int64)]
 
 

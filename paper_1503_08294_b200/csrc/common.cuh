@@ -162,6 +162,10 @@ struct FindArgs {
   int64_t n = 0;                 // rows to scan (host value / upper bound)
   const int* n_dev = nullptr;    // if set: exact row count read on the device
   const double* sig = nullptr;   // m x 3 f64
+  // optional fused sampling: signal j is sig_pts[sig_idx[j]] and the find
+  // writes it to sig (then non-const) for the update that follows
+  const int64_t* sig_idx = nullptr;
+  const double* sig_pts = nullptr;
   int64_t m = 0;
   int64_t* out_idx = nullptr;
   double* out_d2 = nullptr;
@@ -173,5 +177,8 @@ void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work)
 
 // device CloudSource sampler (sample.cu): m signals into d_out on `stream`
 void sampler_draw(gs_sampler* s, int64_t m, double* d_out, cudaStream_t stream);
+// ... or just their cloud indices (the find gathers them); the cloud
+void sampler_indices(gs_sampler* s, int64_t m, int64_t* d_idx, cudaStream_t stream);
+const double* sampler_points(const gs_sampler* s);
 
 }  // namespace gs

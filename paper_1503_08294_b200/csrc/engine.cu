@@ -59,7 +59,7 @@ constexpr int32_t kNone32 = 0x7f7f7f7f;
 constexpr long long kNone64 = 0x7f7f7f7f7f7f7f7fLL;
 constexpr int kRingDisk = 0, kRingHalf = 1, kRingInc = 2;
 #ifndef GS_UPD_THREADS
-#define GS_UPD_THREADS 512
+#define GS_UPD_THREADS 256
 #endif
 constexpr int kUpdThreads = GS_UPD_THREADS;
 constexpr long long kSweepEvery = 1024;  // engine.py:98
@@ -92,7 +92,7 @@ struct Counters {
   int max_degree;
   long long ev_create, ev_insert, ev_prune, ev_sweep;
   long long cyc_serial, cyc_total;
-  long long cyc_phase[8];
+  long long cyc_phase[12];
   int inserted_start;
   int stale_n;
   int converged;
@@ -100,8 +100,6 @@ struct Counters {
   long long ev_cutoff;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
-  long long prof_max[4];  // GS_PROF: per-window max thread cycles (B, walk, C1, A)
-  long long prof_lv[5], prof_lvsum[5];
 };
 
 struct Params {
@@ -845,6 +843,7 @@ struct gs_engine {
   DevBuf find_work;
   DevBuf sig_buf;
   DevBuf rec_buf;
+  DevBuf idx_buf;  // sampled cloud indices (gs_engine_step_sampled)
   gs_batch_stats* h_stats = nullptr;  // pinned
   double* h_sig = nullptr;            // pinned staging for host batches
   size_t h_sig_cap = 0;
@@ -1041,6 +1040,13 @@ long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
 }
 
 void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m) {
+  if constexpr (kCluster > 8) {  // clusters beyond the portable 8 CTAs need an opt-in
+    static bool opted = false;
+    if (!opted) {
+      GS_CUDA(cudaFuncSetAttribute(k_update_batch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      opted = true;
+    }
+  }
   e->batch_no++;
   k_update_batch<<<kCluster, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m, e->batch_no);
   GS_CUDA(cudaGetLastError());
@@ -1048,15 +1054,21 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
   ++g_launches;
 }
 
-void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinRec* d_rec) {
+void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinRec* d_rec,
+                 const int64_t* sig_idx = nullptr, const double* sig_pts = nullptr) {
   GS_CHECK(e->n_units >= 2, GS_STATE_ERROR, "need at least 2 units to find winners");
   FindArgs a;
   a.pos4 = e->S.pos;
   a.rows = e->S.rows;
   a.alive = e->S.alive;
-  a.n = e->next_id;  // host upper bound on the row count (grid sizing)
+  // host estimate of the row count (grid sizing, staging); with batches in
+  // flight it can lag the device's count, which every find kernel reads
+  // (n_dev) and handles past the estimate
+  a.n = e->next_id;
   a.n_dev = &e->S.cnt->nrows;  // exact row count, read on the device
   a.sig = d_sig + 3 * lo;
+  a.sig_idx = sig_idx ? sig_idx + lo : nullptr;
+  a.sig_pts = sig_pts;
   a.m = hi - lo;
   a.out_win = d_rec + lo;
   a.mode = e->hp.find_mode;
@@ -1157,6 +1169,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   e->find_work.release();
   e->sig_buf.release();
   e->rec_buf.release();
+  e->idx_buf.release();
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -1269,24 +1282,31 @@ extern "C" gs_status gs_engine_set_unit(gs_engine* e, int64_t id, const double* 
   });
 }
 
+namespace {
+// find + update for one batch on the engine stream.  With sig_idx the find
+// gathers the signals from the sampler's cloud into d_sig (fused sampling).
+void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_t* sig_idx,
+                      const double* sig_pts) {
+  GS_CHECK(e && d_sig && m > 0, GS_VALUE_ERROR, "bad step arguments");
+  GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
+  ensure_capacity(e, m, 3 * m);
+  WinRec* rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
+  const bool timed = e->timing && !e->ev_pending;
+  if (timed) GS_CUDA(cudaEventRecord(e->ev[0], e->stream));
+  launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
+  if (timed) GS_CUDA(cudaEventRecord(e->ev[1], e->stream));
+  launch_update(e, d_sig, rec, m);
+  if (timed) {
+    GS_CUDA(cudaEventRecord(e->ev[2], e->stream));
+    e->ev_pending = true;
+  }
+  GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
+                          cudaMemcpyDeviceToHost, e->stream));
+}
+}  // namespace
+
 extern "C" gs_status gs_engine_step_device(gs_engine* e, const double* d_sig, int64_t m) {
-  return guarded([&] {
-    GS_CHECK(e && d_sig && m > 0, GS_VALUE_ERROR, "bad step arguments");
-    GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
-    ensure_capacity(e, m, 3 * m);
-    WinRec* rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
-    const bool timed = e->timing && !e->ev_pending;
-    if (timed) GS_CUDA(cudaEventRecord(e->ev[0], e->stream));
-    launch_find(e, d_sig, 0, m, rec);
-    if (timed) GS_CUDA(cudaEventRecord(e->ev[1], e->stream));
-    launch_update(e, d_sig, rec, m);
-    if (timed) {
-      GS_CUDA(cudaEventRecord(e->ev[2], e->stream));
-      e->ev_pending = true;
-    }
-    GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
-                            cudaMemcpyDeviceToHost, e->stream));
-  });
+  return guarded([&] { step_device_impl(e, d_sig, m, nullptr, nullptr); });
 }
 
 namespace {
@@ -1328,15 +1348,19 @@ extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
 // One iteration whose m signals are drawn on the device by a CloudSource
 // sampler (sample.cu) into the engine's signal buffer; out != NULL makes it
 // synchronous (stats copied out), else it stays queued on the engine stream.
+// One iteration whose m signals are drawn on the device by a CloudSource
+// sampler (sample.cu): the sampler kernel emits cloud indices, the find
+// gathers the points into the engine's signal buffer as it loads them.
+// out != NULL makes it synchronous (stats copied out), else it stays queued.
 extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64_t m,
                                             gs_batch_stats* out) {
   return guarded([&] {
     GS_CHECK(e && smp && m > 0, GS_VALUE_ERROR, "bad step arguments");
     double* d_sig = (double*)e->sig_buf.get(sizeof(double) * 3 * (size_t)m);
-    sampler_draw(smp, m, d_sig, e->stream);
+    int64_t* d_idx = (int64_t*)e->idx_buf.get(sizeof(int64_t) * (size_t)m);
+    sampler_indices(smp, m, d_idx, e->stream);
     e->launches++;
-    gs_status st = gs_engine_step_device(e, d_sig, m);
-    if (st != GS_OK) throw Fail{st};
+    step_device_impl(e, d_sig, m, d_idx, sampler_points(smp));
     if (out) {
       GS_CUDA(cudaStreamSynchronize(e->stream));
       harvest_timing(e);

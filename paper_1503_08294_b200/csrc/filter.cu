@@ -60,6 +60,8 @@ struct FilterMeta {
   unsigned int nlive;          // live rows scanned
   unsigned int nfb;            // fallback list length (signals the filter could not certify)
   unsigned int nexact;         // listed signals that also needed the FP64 scan
+  unsigned int overflow;       // more rows than the pair array holds (host estimate stale):
+                               // every signal takes the exact FP64 scan
 };
 
 struct Top3 {
@@ -109,6 +111,7 @@ __global__ void k_filter_init(FilterMeta* M, int* hist) {
     M->nfb = 0u;
     M->nlive = 0u;
     M->nexact = 0u;
+    M->overflow = 0u;
   }
 }
 
@@ -164,6 +167,7 @@ __global__ void k_prep(FindArgs a, FilterMeta* M, UPair* U, int64_t npairs_alloc
     M->cx = cx;
     M->cy = cy;
     M->cz = cz;
+    if (nrows > 2 * npairs_alloc) M->overflow = 1u;
   }
   float pm = 0.f;
   unsigned live = 0;
@@ -401,7 +405,7 @@ __device__ void certify(const FindArgs& a, const FilterMeta* M, int64_t j, const
   const double Q = sqrt(q2);
   const double pmax = (double)__uint_as_float(M->pmax_bits);
   // FP32 values stay far from overflow below 1e30; beyond it, go exact
-  bool ok = pmax * pmax <= 1e30 && q2 <= 1e30;
+  bool ok = pmax * pmax <= 1e30 && q2 <= 1e30 && !M->overflow;
   if (t.i3 < 0) {
     // fewer than three finite FP32 values: certified only if every live
     // row is among the candidates
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(FindArgs a, const Filte
     const float fx = __double2float_rn(Qx), fy = __double2float_rn(Qy), fz = __double2float_rn(Qz);
     Top3 t;
     top3_init(t);
-    for (int64_t p = threadIdx.x; p < npairs; p += kFbThreads) {
+    for (int64_t p = threadIdx.x; p < (M->overflow ? 0 : npairs); p += kFbThreads) {
       const UPair u = U[p];
       if (u.w0 != INFINITY) {
         const float dx = -0.5f * u.ax0 - fx, dy = -0.5f * u.ay0 - fy, dz = -0.5f * u.az0 - fz;
@@ -733,7 +737,7 @@ __global__ void __launch_bounds__(kFbThreads) k_fallback(FindArgs a, const Filte
       if (c1 >= 0) b.push(d1 = exact_d2(a, nrows, c1, qx, qy, qz), c1);
       const double q2 = Qx * Qx + Qy * Qy + Qz * Qz;
       const double R = (double)__uint_as_float(M->pmax_bits) + sqrt(q2);
-      bool ok = R * R <= 1e30;
+      bool ok = R * R <= 1e30 && !M->overflow;
       if (m.i3 < 0) {
         ok = ok && M->nlive == (unsigned)((c0 >= 0) + (c1 >= 0));
       } else if (ok) {

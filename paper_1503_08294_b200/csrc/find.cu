@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kFT) find_exact_kernel(FindArgs a, int64_t row
   const int64_t sig0 = (int64_t)blockIdx.x * (kFT * kFS);
   const int64_t r_begin = (int64_t)blockIdx.y * rows_per_chunk;
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
-  const int64_t r_end = min(n, r_begin + rows_per_chunk);
+  // the last chunk takes every row past the host's estimate
+  const int64_t r_end = blockIdx.y + 1 == gridDim.y ? n : min(n, r_begin + rows_per_chunk);
 
   double qx[kFS], qy[kFS], qz[kFS];
   Best2 best[kFS];
@@ -166,22 +167,13 @@ __device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
 }
 
 template <int kFS>
-__global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a) {
-  extern __shared__ double s_rows[];  // [3][nr]
+__global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, int tile_rows) {
+  extern __shared__ double s_rows[];  // [3][tile_rows]
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
-  const int nr = (int)n;
   double* sx = s_rows;
-  double* sy = s_rows + nr;
-  double* sz = s_rows + 2 * nr;
+  double* sy = s_rows + tile_rows;
+  double* sz = s_rows + 2 * tile_rows;
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  for (int r = threadIdx.x; r < nr; r += kSmallThreads) {
-    double x = kInf, y = kInf, z = kInf;
-    if (!load_row(a, r, x, y, z)) x = y = z = kInf;
-    sx[r] = x;
-    sy[r] = y;
-    sz[r] = z;
-  }
-  __syncthreads();
   const int slice = threadIdx.x & (kSmallSlices - 1);
   const int sl = threadIdx.x / kSmallSlices;  // 0..15
   const int64_t sig0 = (int64_t)blockIdx.x * (kSmallThreads / kSmallSlices) * kFS;
@@ -193,15 +185,43 @@ __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a) {
     b[k].init();
     qx[k] = qy[k] = qz[k] = 0.0;
     if (j < a.m) {
-      qx[k] = a.sig[3 * j];
-      qy[k] = a.sig[3 * j + 1];
-      qz[k] = a.sig[3 * j + 2];
+      if (a.sig_idx) {  // fused sampling: gather the signal, one lane stores it
+        const size_t src = 3 * (size_t)a.sig_idx[j];
+        qx[k] = a.sig_pts[src];
+        qy[k] = a.sig_pts[src + 1];
+        qz[k] = a.sig_pts[src + 2];
+        if (slice == 0) {
+          double* o = const_cast<double*>(a.sig);
+          o[3 * j] = qx[k];
+          o[3 * j + 1] = qy[k];
+          o[3 * j + 2] = qz[k];
+        }
+      } else {
+        qx[k] = a.sig[3 * j];
+        qy[k] = a.sig[3 * j + 1];
+        qz[k] = a.sig[3 * j + 2];
+      }
     }
   }
-  for (int r = slice; r < nr; r += kSmallSlices) {
-    const double px = sx[r], py = sy[r], pz = sz[r];
+  // one tile in the common case; more when the device's row count has grown
+  // past the host's estimate (batches in flight)
+  for (int64_t t0 = 0; t0 < n; t0 += tile_rows) {
+    const int nr = (int)min((int64_t)tile_rows, n - t0);
+    if (t0 > 0) __syncthreads();
+    for (int r = threadIdx.x; r < nr; r += kSmallThreads) {
+      double x = kInf, y = kInf, z = kInf;
+      if (!load_row(a, t0 + r, x, y, z)) x = y = z = kInf;
+      sx[r] = x;
+      sy[r] = y;
+      sz[r] = z;
+    }
+    __syncthreads();
+    for (int r = slice; r < nr; r += kSmallSlices) {
+      const double px = sx[r], py = sy[r], pz = sz[r];
 #pragma unroll
-    for (int k = 0; k < kFS; ++k) b[k].push(dist2_exact(px, py, pz, qx[k], qy[k], qz[k]), r);
+      for (int k = 0; k < kFS; ++k)
+        b[k].push(dist2_exact(px, py, pz, qx[k], qy[k], qz[k]), (int32_t)(t0 + r));
+    }
   }
 #pragma unroll
   for (int k = 0; k < kFS; ++k) {
@@ -219,11 +239,33 @@ __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a) {
   }
 }
 
+// materialise sampled signals (sig[j] = pts[idx[j]]) for the non-fused finds
+__global__ void k_gather_signals(const int64_t* idx, const double* pts, double* sig, int64_t m) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const size_t src = 3 * (size_t)idx[j];
+  sig[3 * j] = pts[src];
+  sig[3 * j + 1] = pts[src + 1];
+  sig[3 * j + 2] = pts[src + 2];
+}
+
 // forward declaration (filter.cu)
 bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 
-void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work) {
-  if (a.m <= 0) return;
+void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& work) {
+  if (a_in.m <= 0) return;
+  FindArgs a = a_in;
+  const bool small = a.n <= kSmallMaxRows &&
+                     !((a.mode == GS_FIND_FILTER) || (a.mode == GS_FIND_AUTO && a.n >= 4096 &&
+                                                      (double)a.n * (double)a.m >= 6.0e7));
+  if (a.sig_idx && !small) {  // only the small kernel gathers in place
+    k_gather_signals<<<(unsigned)((a.m + 255) / 256), 256, 0, stream>>>(
+        a.sig_idx, a.sig_pts, const_cast<double*>(a.sig), a.m);
+    GS_CUDA(cudaGetLastError());
+    ++g_launches;
+    a.sig_idx = nullptr;
+    a.sig_pts = nullptr;
+  }
   if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
       find_filter_launch(ctx, a, stream, work))
     return;
@@ -237,13 +279,16 @@ void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work)
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       attr_set = true;
     }
-    const size_t smem = 24 * (size_t)std::max<int64_t>(a.n, 1);
+    // rows staged per tile: the estimate plus headroom for growth in flight
+    const int tile_rows = (int)std::min<int64_t>(kSmallMaxRows, std::max<int64_t>(a.n, 1) + 512);
+    const size_t smem = 24 * (size_t)tile_rows;
     const int64_t per1 = kSmallThreads / kSmallSlices;
     if (a.m >= 8LL * ctx.sm_count * per1 * 4) {
       find_small_kernel<4><<<(unsigned)((a.m + 4 * per1 - 1) / (4 * per1)), kSmallThreads, smem,
-                             stream>>>(a);
+                             stream>>>(a, tile_rows);
     } else {
-      find_small_kernel<1><<<(unsigned)((a.m + per1 - 1) / per1), kSmallThreads, smem, stream>>>(a);
+      find_small_kernel<1><<<(unsigned)((a.m + per1 - 1) / per1), kSmallThreads, smem, stream>>>(
+          a, tile_rows);
     }
     GS_CUDA(cudaGetLastError());
     ++g_launches;

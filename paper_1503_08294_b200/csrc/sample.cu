@@ -113,13 +113,20 @@ __device__ void advance_state(PhiloxState& s, unsigned long long C) {
 }
 
 constexpr int kSampThreads = 1024;
-constexpr int kSampPer = 8;  // consecutive draws per thread per round
+constexpr int kSampPer = 8;  // one Philox block (4 words = 8 draws) per thread per round
 
+// One CTA per batch.  The stream after the state's position is: the pending
+// high half (if any), the halves of the buffered words, then whole Philox
+// blocks ctr+1, ctr+2, ...  Thread 0 handles that short prefix (<= 9
+// draws); then every thread computes ONE block per round -- eight
+// consecutive draws -- the rare rejections are flagged, a block scan ranks
+// the accepted draws in stream order, and the first m gather points[idx].
 __global__ void __launch_bounds__(kSampThreads) k_cloud_sample(PhiloxState* st, const double* pts,
                                                                unsigned npts, int m,
                                                                double* out, int64_t* out_idx) {
   __shared__ int s_warp[32];
   __shared__ int s_total;
+  __shared__ int s_pre;
   __shared__ unsigned long long s_consumed;
   if (npts == 1u) {  // integers(0, 1) returns zeros without drawing
     for (int j = threadIdx.x; j < m; j += kSampThreads) {
@@ -137,36 +144,72 @@ __global__ void __launch_bounds__(kSampThreads) k_cloud_sample(PhiloxState* st, 
   const unsigned excl = npts;
   const unsigned thr = (0xffffffffu - rng) % excl;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  int produced = 0;
-  unsigned long long base = 0;
-  if (tid == 0) s_consumed = 0;
-  while (produced < m) {  // uniform: produced is block-wide
+  auto emit = [&](int rank, unsigned v) {
+    if (out) {
+      const size_t p = (size_t)v * 3;
+      out[3 * (size_t)rank] = pts[p];
+      out[3 * (size_t)rank + 1] = pts[p + 1];
+      out[3 * (size_t)rank + 2] = pts[p + 2];
+    }
+    if (out_idx) out_idx[rank] = (int64_t)v;
+  };
+  // ---- prefix: pending half + buffered words (no Philox needed)
+  const int npre = s.has + 2 * (4 - s.pos);
+  if (tid == 0) {
+    int produced = 0;
+    s_consumed = 0;
+    for (int i = 0; i < npre && produced < m; ++i) {
+      unsigned u32;
+      if (s.has && i == 0) {
+        u32 = s.u;
+      } else {
+        const int k = i - s.has;
+        const unsigned long long word = s.buf[s.pos + (k >> 1)];
+        u32 = (k & 1) ? (unsigned)(word >> 32) : (unsigned)word;
+      }
+      const unsigned long long mm = (unsigned long long)u32 * excl;
+      if ((unsigned)mm >= thr) {
+        emit(produced, (unsigned)(mm >> 32));
+        if (++produced == m) s_consumed = (unsigned long long)i + 1;
+      }
+    }
+    s_pre = produced;
+  }
+  __syncthreads();
+  int produced = s_pre;
+  unsigned long long block0 = 0;  // blocks already handed out (ctr + 1 + block index)
+  while (produced < m) {          // uniform: produced is block-wide
+    const unsigned long long b = block0 + (unsigned long long)tid;
+    unsigned long long c[4], o[4];
+    ctr_add(s.ctr, b + 1, c);
+    philox4x64_10(c, s.key, o);
     unsigned vals[kSampPer];
     unsigned acc = 0;  // bit e: draw e accepted
 #pragma unroll
     for (int e = 0; e < kSampPer; ++e) {
-      const unsigned long long i = base + (unsigned long long)tid * kSampPer + e;
-      const unsigned long long mm = (unsigned long long)stream_u32(s, i) * excl;
+      const unsigned long long word = o[e >> 1];
+      const unsigned u32 = (e & 1) ? (unsigned)(word >> 32) : (unsigned)word;
+      const unsigned long long mm = (unsigned long long)u32 * excl;
       vals[e] = (unsigned)(mm >> 32);
-      if ((unsigned)(mm & 0xffffffffULL) >= thr) acc |= 1u << e;
+      if ((unsigned)mm >= thr) acc |= 1u << e;
     }
-    // block exclusive scan of accepted counts (thread order == draw order)
+    // block exclusive scan of accepted counts (thread order == stream order)
     const int cnt = __popc(acc);
     int inc = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o2);
+      if (lane >= o2) inc += t;
     }
     if (lane == 31) s_warp[w] = inc;
     __syncthreads();
     if (w == 0) {
-      int x = s_warp[lane];
+      const int x = s_warp[lane];
       int xi = x;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, xi, o);
-        if (lane >= o) xi += t;
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, xi, o2);
+        if (lane >= o2) xi += t;
       }
       s_warp[lane] = xi - x;
       if (lane == 31) s_total = xi;
@@ -177,19 +220,13 @@ __global__ void __launch_bounds__(kSampThreads) k_cloud_sample(PhiloxState* st, 
     for (int e = 0; e < kSampPer; ++e) {
       if (!((acc >> e) & 1u)) continue;
       if (rank < m) {
-        if (out) {
-          const size_t p = (size_t)vals[e] * 3;
-          out[3 * (size_t)rank] = pts[p];
-          out[3 * (size_t)rank + 1] = pts[p + 1];
-          out[3 * (size_t)rank + 2] = pts[p + 2];
-        }
-        if (out_idx) out_idx[rank] = (int64_t)vals[e];
-        if (rank == m - 1) s_consumed = base + (unsigned long long)tid * kSampPer + e + 1;
+        emit(rank, vals[e]);
+        if (rank == m - 1) s_consumed = (unsigned long long)npre + b * kSampPer + e + 1;
       }
       ++rank;
     }
     produced += s_total;
-    base += (unsigned long long)kSampThreads * kSampPer;
+    block0 += kSampThreads;
     __syncthreads();
   }
   if (tid == 0) {
@@ -209,7 +246,19 @@ struct gs_sampler {
   unsigned long long npts = 0;
   PhiloxState* d_state = nullptr;
   bool owns_pts = false;
+  gs::DevBuf idx_tmp;  // indices for gs_sampler_draw's parallel gather
 };
+
+namespace gs {
+__global__ void k_sample_gather(const int64_t* idx, const double* pts, double* out, int64_t m) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const size_t src = 3 * (size_t)idx[j];
+  out[3 * j] = pts[src];
+  out[3 * j + 1] = pts[src + 1];
+  out[3 * j + 2] = pts[src + 2];
+}
+}  // namespace gs
 
 extern "C" gs_status gs_sampler_create(gs_ctx* ctx, const double* points, int64_t npts,
                                        int points_on_device, gs_sampler** out) {
@@ -249,6 +298,7 @@ extern "C" void gs_sampler_destroy(gs_sampler* s) {
   cudaSetDevice(s->ctx->device);
   if (s->d_state) cudaFree(s->d_state);
   if (s->owns_pts && s->d_pts) cudaFree(s->d_pts);
+  s->idx_tmp.release();
   delete s;
 }
 
@@ -299,11 +349,25 @@ static void sampler_launch(gs_sampler* s, int64_t m, double* d_out, int64_t* d_i
   ++g_launches;
 }
 
+// indices from the one-CTA generator, then a full-grid gather
 void gs::sampler_draw(gs_sampler* s, int64_t m, double* d_out, cudaStream_t st) {
   GS_CHECK(s && d_out, GS_VALUE_ERROR, "null argument");
   GS_CHECK(s->d_pts, GS_VALUE_ERROR, "index-only sampler has no points");
-  sampler_launch(s, m, d_out, nullptr, st);
+  if (m <= 0) return;
+  int64_t* idx = (int64_t*)s->idx_tmp.get(sizeof(int64_t) * (size_t)m);
+  sampler_launch(s, m, nullptr, idx, st);
+  k_sample_gather<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(idx, s->d_pts, d_out, m);
+  GS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
+
+void gs::sampler_indices(gs_sampler* s, int64_t m, int64_t* d_idx, cudaStream_t st) {
+  GS_CHECK(s && d_idx, GS_VALUE_ERROR, "null argument");
+  GS_CHECK(s->d_pts, GS_VALUE_ERROR, "index-only sampler has no points");
+  sampler_launch(s, m, nullptr, d_idx, st);
+}
+
+const double* gs::sampler_points(const gs_sampler* s) { return s->d_pts; }
 
 extern "C" gs_status gs_sampler_draw_indices(gs_sampler* s, int64_t m, int64_t* d_idx,
                                              void* stream) {

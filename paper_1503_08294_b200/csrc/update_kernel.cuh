@@ -70,28 +70,34 @@ __device__ void walk_unit(const DevState& S, const Params& P, const double* sig,
   const double h0 = S.hab[u];
   double h = h0;
   constexpr int kNone = 0x7fffffff;
-  if (d <= kStage) {
-    int2 nb[kStage];
-    stage_adj(A, d, nb);
-    int key[kStage + 1];
+  if (d <= 2 * kStage) {
+    // up to 2*kStage neighbours: keys staged in registers, two chunks of loads
+    constexpr int kK = 2 * kStage;
+    int key[kK + 1];
 #pragma unroll
-    for (int k = 0; k < kStage; ++k) {
-      const int jw = k < d ? S.firstwin[nb[k].x] : kNone;
-      key[k] = jw < jstar ? (jw << 1) : kNone;
+    for (int c = 0; c < 2; ++c) {
+      int2 nb[kStage];
+      const int dc = min(kStage, d - c * kStage);
+      stage_adj(A + c * kStage, dc, nb);
+#pragma unroll
+      for (int k = 0; k < kStage; ++k) {
+        const int jw = k < dc ? S.firstwin[nb[k].x] : kNone;
+        key[c * kStage + k] = jw < jstar ? (jw << 1) : kNone;
+      }
     }
-    key[kStage] = jself < jstar ? ((jself << 1) | 1) : kNone;
+    key[kK] = jself < jstar ? ((jself << 1) | 1) : kNone;
     // four events per group: their signal loads issue together
     int last = -1;
 #pragma unroll 1
-    for (int grp = 0; grp < (kStage + 4) / 4; ++grp) {
+    for (int grp = 0; grp < (kK + 4) / 4; ++grp) {
       int cur[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        int c = kNone;
+        int cc = kNone;
 #pragma unroll
-        for (int k = 0; k <= kStage; ++k) c = (key[k] > last && key[k] < c) ? key[k] : c;
-        cur[q] = c;
-        if (c != kNone) last = c;
+        for (int k = 0; k <= kK; ++k) cc = (key[k] > last && key[k] < cc) ? key[k] : cc;
+        cur[q] = cc;
+        if (cc != kNone) last = cc;
       }
       double xs[4], ys[4], zs[4];
 #pragma unroll
@@ -182,14 +188,21 @@ __device__ int classify_ring_warp(const DevState& S, int u, int* sh) {
     const int v = sh[lane];
     const int dv = S.deg[v];
     const int2* V = S.adj + (size_t)v * kMaxDeg;
-    for (int c = 0; c < dv && d <= 2; ++c) {
-      const int w = V[c].x;
-      for (int i = 0; i < k; ++i)
-        if (sh[i] == w) {
-          ++d;
-          mask |= 1u << i;
-          break;
-        }
+    // v's row in staged chunks (loads issue together), membership against N(u)
+    for (int c0 = 0; c0 < dv && d <= 2; c0 += kStage) {
+      int2 nb[kStage];
+      stage_adj(V + c0, min(kStage, dv - c0), nb);
+#pragma unroll
+      for (int c = 0; c < kStage; ++c) {
+        if (c0 + c >= dv || d > 2) continue;
+        const int w = nb[c].x;
+        for (int i = 0; i < k; ++i)
+          if (sh[i] == w) {
+            ++d;
+            mask |= 1u << i;
+            break;
+          }
+      }
     }
   }
   const bool bad = lane < k && (d == 0 || d > 2);
@@ -251,12 +264,267 @@ __device__ int event_part1b(const DevState& S, const Params& P, int b, int s, do
 }
 
 // ---------------------------------------------------------------------------
+// Warp-cooperative event path.  The event signal runs update_single's
+// topology work on one warp: every lane calls these with the same
+// arguments, adjacency rows are scanned lane-parallel (one dependent load
+// level instead of a per-entry chain), lane 0 performs the scalar updates
+// in the reference's order, and __syncwarp orders them for the other lanes.
+// Ring recomputes are deferred (S.defer_n set), exactly as in the serial
+// primitives they replace (engine.cu: find_slot, connect_or_reset,
+// remove_edge, age_incident, prune_winner; network.py:261-369).
+
+// slot of b in a's adjacency, or -1 (uniform)
+__device__ int w_find_slot(const DevState& S, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  const int d = S.deg[a];
+  const int2* A = S.adj + (size_t)a * kMaxDeg;
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    const int k = k0 + lane;
+    const unsigned bal = __ballot_sync(0xffffffffu, k < d && A[k].x == b);
+    if (bal) return k0 + __ffs(bal) - 1;
+  }
+  return -1;
+}
+
+// deferred _recompute_ring for u (each unit queued once; lanes may call it
+// concurrently for different units)
+__device__ __forceinline__ void w_defer(const DevState& S, int u) {
+  if (atomicExch(&S.touchfirst[u], -2) != -2) {
+    const int k = atomicAdd(S.defer_n, 1);
+    if (k < kDeferCap) S.defer_list[k] = u;
+    else set_err(S, E_AFF);
+  }
+}
+
+// defer the rings of _ring_neighborhood(a, b) (network.py:424-433): the
+// common neighbours of a and b, then a and b.  stage: per-warp smem (64 ints)
+__device__ void w_defer_ring_neighborhood(const DevState& S, int a, int b, int* stage) {
+  const int lane = threadIdx.x & 31;
+  const int db = S.deg[b];
+  const int2* Bb = S.adj + (size_t)b * kMaxDeg;
+  for (int k = lane; k < db; k += 32) stage[k] = Bb[k].x;
+  __syncwarp();
+  const int da = S.deg[a];
+  const int2* Aa = S.adj + (size_t)a * kMaxDeg;
+  for (int k = lane; k < da; k += 32) {
+    const int v = Aa[k].x;
+    bool common = false;
+    if (v != b)
+      for (int q = 0; q < db; ++q) common |= stage[q] == v;
+    if (common) w_defer(S, v);
+  }
+  if (lane == 0) {
+    w_defer(S, a);
+    w_defer(S, b);
+  }
+  __syncwarp();
+}
+
+// connect_or_reset (network.py:261-282): 1 created, 0 reset, -1 error (uniform)
+__device__ int w_connect_or_reset(const DevState& S, int a, int b, int* stage) {
+  const int lane = threadIdx.x & 31;
+  const int k = w_find_slot(S, a, b);
+  if (k >= 0) {
+    if (lane == 0) S.eage[S.adj[(size_t)a * kMaxDeg + k].y] = 0;
+    __syncwarp();
+    return 0;
+  }
+  int ok = 0;
+  if (lane == 0) {
+    Counters* c = S.cnt;
+    if (S.deg[a] >= kMaxDeg || S.deg[b] >= kMaxDeg) {
+      set_err(S, E_DEGREE);
+    } else if (c->efree_top <= 0) {
+      set_err(S, E_EDGE_CAP);
+    } else {
+      const int e = S.efree[--c->efree_top];
+      S.eage[e] = 0;
+      if (S.deg[a] == 0) iso_del(S, a);
+      if (S.deg[b] == 0) iso_del(S, b);
+      S.adj[(size_t)a * kMaxDeg + S.deg[a]++] = make_int2(b, e);
+      S.adj[(size_t)b * kMaxDeg + S.deg[b]++] = make_int2(a, e);
+      c->n_edges++;
+      const int dm = max(S.deg[a], S.deg[b]);
+      if (dm > c->max_degree) c->max_degree = dm;
+      ok = 1;
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __syncwarp();
+  if (!ok) return -1;
+  w_defer_ring_neighborhood(S, a, b, stage);
+  return 1;
+}
+
+// _remove_edge_raw (network.py:453-462)
+__device__ void w_remove_edge_raw(const DevState& S, int a, int b) {
+  const int lane = threadIdx.x & 31;
+  const int ka = w_find_slot(S, a, b);
+  const int kb = w_find_slot(S, b, a);
+  if (lane == 0) {
+    if (ka < 0 || kb < 0) {
+      set_err(S, E_NOEDGE);
+    } else {
+      Counters* c = S.cnt;
+      int2* A = S.adj + (size_t)a * kMaxDeg;
+      int2* B = S.adj + (size_t)b * kMaxDeg;
+      const int e = A[ka].y;
+      const int da = --S.deg[a];
+      A[ka] = A[da];
+      const int db = --S.deg[b];
+      B[kb] = B[db];
+      S.efree[c->efree_top++] = e;
+      c->n_edges--;
+      if (da == 0) iso_add(S, a);
+      if (db == 0) iso_add(S, b);
+    }
+  }
+  __syncwarp();
+}
+
+// age_incident_edges(b, inc, exclude) with the over-age registry
+// (network.py:294-319); crossing neighbours land in over[] in adjacency order
+__device__ void w_age_incident(const DevState& S, const Params& P, int b, int exclude, int inc,
+                               int* over, int* nover) {
+  const int lane = threadIdx.x & 31;
+  const int d = S.deg[b];
+  const int2* B = S.adj + (size_t)b * kMaxDeg;
+  int n = 0;
+  for (int k0 = 0; k0 < d; k0 += 32) {
+    const int k = k0 + lane;
+    bool cross = false;
+    int v = -1;
+    if (k < d) {
+      const int2 ent = B[k];
+      v = ent.x;
+      if (v != exclude) {
+        const int old = S.eage[ent.y];
+        const int nw = old + inc;
+        S.eage[ent.y] = nw;
+        cross = nw > P.max_age && old <= P.max_age;
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cross);
+    if (cross) over[n + __popc(bal & ((1u << lane) - 1u))] = v;
+    n += __popc(bal);
+  }
+  if (lane == 0) *nover = n;
+  __syncwarp();
+}
+
+// prune on the winner's over-age edges (network.py:321-369), as prune_winner
+__device__ void w_prune_winner(const DevState& S, const Params& P, int b, const int* over,
+                               int nover, int* stage, int* pe, int* pu) {
+  const int lane = threadIdx.x & 31;
+  *pe = 0;
+  *pu = 0;
+  if (nover == 0 && S.cnt->iso_count == 0) return;
+  for (int i = 0; i < nover; ++i) {
+    w_defer_ring_neighborhood(S, b, over[i], stage);
+    w_remove_edge_raw(S, b, over[i]);
+  }
+  int removed = 0;
+  if (lane == 0) removed = remove_lonely(S, P);
+  *pu = __shfl_sync(0xffffffffu, removed, 0);
+  *pe = nover;
+  __syncwarp();
+}
+
+// sweep clock (no stale units to remove) + adapt_threshold (engine.py:208-238,
+// 345-355), whole warp: the neighbours' habituation is checked lane-parallel
+__device__ void w_event_part2(const DevState& S, const Params& P, int b, bool sweep_fired) {
+  const int lane = threadIdx.x & 31;
+  Counters* c = S.cnt;
+  if (lane == 0 && sweep_fired) c->next_sweep = c->tick + kSweepEvery;
+  if (!S.alive[b]) return;
+  const int ring = S.ring[b];
+  if (ring == kRingDisk || (P.allow_boundary && ring == kRingHalf)) {
+    if (lane == 0) S.patience[b] = 0;
+    return;
+  }
+  if (S.hab[b] >= P.h_t) return;
+  const int d = S.deg[b];
+  const int2* B = S.adj + (size_t)b * kMaxDeg;
+  bool untrained = false;
+  for (int k = lane; k < d; k += 32) untrained |= S.hab[B[k].x] >= P.h_t;
+  if (__any_sync(0xffffffffu, untrained)) return;
+  if (lane == 0) {
+    int count = S.patience[b] + 1;
+    if (count >= P.ring_patience) {
+      S.theta[b] = dmul(S.theta[b], P.rho);
+      count = 0;
+    }
+    S.patience[b] = count;
+  }
+}
+
+// update_single up to the edge aging (engine.py:303-308), whole warp
+__device__ void w_event_part1a(const DevState& S, const Params& P, int b, int s, int* over,
+                               int* nover, int* stage) {
+  const int lane = threadIdx.x & 31;
+  Counters* c = S.cnt;
+  if (lane == 0) {
+    const long long tick = ++c->tick;
+    touch_active(S, b, tick, 0);
+    touch_active(S, s, tick, 1);
+  }
+  __syncwarp();
+  const int created = w_connect_or_reset(S, b, s, stage);
+  if (lane == 0) {
+    if (created > 0) c->ev_create++;
+    *nover = 0;
+  }
+  __syncwarp();
+  if (created >= 0) w_age_incident(S, P, b, s, 1, over, nover);
+}
+
+// maybe_insert + prune (engine.py:335-344), whole warp; 1 when the sweep
+// clock fired (uniform)
+__device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, double dw,
+                              double x, double y, double z, const int* over, int nover,
+                              int* stage) {
+  const int lane = threadIdx.x & 31;
+  Counters* c = S.cnt;
+  const long long tick = c->tick;
+  if (dw > S.theta[b] && S.hab[b] < P.h_t) {
+    int r = -1;
+    if (lane == 0) {
+      const double4 wp = S.pos[b];
+      r = add_unit(S, P, dmul(dadd(wp.x, x), 0.5), dmul(dadd(wp.y, y), 0.5),
+                   dmul(dadd(wp.z, z), 0.5), S.theta[b]);
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    __syncwarp();
+    if (r < 0) return 0;
+    w_connect_or_reset(S, r, b, stage);
+    w_connect_or_reset(S, r, s, stage);
+    if (w_find_slot(S, b, s) >= 0) {
+      w_defer_ring_neighborhood(S, b, s, stage);
+      w_remove_edge_raw(S, b, s);
+    }
+    if (lane == 0) {
+      touch_active(S, r, tick, 2);
+      c->ev_insert++;
+    }
+    __syncwarp();
+  }
+  int pe, pu;
+  w_prune_winner(S, P, b, over, nover, stage, &pe, &pu);
+  int fired = 0;
+  if (lane == 0) {
+    if (pe || pu) c->ev_prune++;
+    fired = tick >= c->next_sweep ? 1 : 0;
+  }
+  return __shfl_sync(0xffffffffu, fired, 0);
+}
+
+// ---------------------------------------------------------------------------
 // cluster primitives: kCluster CTAs x 1024 threads cooperate on one window;
 // cross-CTA values travel through distributed shared memory and every
 // exchange is fenced by the hardware cluster barrier.
 
 #ifndef GS_CLUSTER
-#define GS_CLUSTER 8
+#define GS_CLUSTER 16
 #endif
 constexpr int kCluster = GS_CLUSTER;
 
@@ -370,6 +638,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_i[8];
   __shared__ int s_over[kMaxDeg];
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
+  __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
   Counters* c = S.cnt;
   const int tid = threadIdx.x;
@@ -428,22 +697,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       dst[rank % kUpdThreads] = j;
     }
     csync();
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[1] += t_ - t_ph; t_ph = t_; }
+    if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
     // ---- B: events and adapt_threshold outcomes; thread g owns rank g
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     int evr = 0x7fffffff;
-#ifdef GS_PROF
-    const long long tb0 = clock64();
-#define GS_TS(var, dep) long long var; asm volatile("mov.u64 %0, %%clock64;" : "=l"(var) : "r"((int)(dep)) : "memory")
-#endif
     if (g < nproc) {
       const int r = g;
       const int jj = s_plist[tid];
       const WinRec w = rec[jj];
       const int b = w.b, s = w.s;
-#ifdef GS_PROF
-      GS_TS(t1, b);
-#endif
       const long long tick_j = tick0 + r + 1;
       bool ev = iso;
       if (tick_j >= next_sweep && ((tick_j - next_sweep) % kSweepEvery) == 0) {
@@ -460,39 +722,29 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       const bool b_trained = hbT < P.h_t;
       bool found = false;
       int kcn = 0;
-#ifdef GS_PROF
-      GS_TS(t2, db + (int)la_b + (int)thb + (int)hbT);
-      long long t3 = t2, t4 = t2, t5 = t2;
-#endif
-      if (db <= kStage) {
+      // the adjacency in chunks of kStage entries: each chunk's loads issue
+      // together (any degree, no dependent per-entry chains)
+      for (int c0 = 0; c0 < db; c0 += kStage) {
+        const int dc = min(kStage, db - c0);
         int2 nb[kStage];
-        stage_adj(B, db, nb);
-#ifdef GS_PROF
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t3) : "r"(nb[0].x + nb[db > 1 ? 1 : 0].y) : "memory");
-#endif
+        stage_adj(B + c0, dc, nb);
         int age[kStage], jv[kStage];
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          const bool valid = k < db, is_s = nb[k].x == s;
+          const bool valid = k < dc, is_s = nb[k].x == s;
           found |= valid && is_s;
           age[k] = (valid && !is_s) ? S.eage[nb[k].y] : 0;
           jv[k] = valid ? S.firstwin[nb[k].x] : kNone32;
         }
-#ifdef GS_PROF
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t4) : "r"(jv[0] + age[0] + jv[db > 1 ? 1 : 0]) : "memory");
-#endif
         int sv[kStage];
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          const bool risk = k < db && nb[k].x != s && age[k] + 2 > P.max_age;
+          const bool risk = k < dc && nb[k].x != s && age[k] + 2 > P.max_age;
           sv[k] = (risk && jv[k] < jj) ? rec[jv[k]].s : -1;
         }
-#ifdef GS_PROF
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t5) : "r"(sv[0] + sv[1]) : "memory");
-#endif
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          if (k >= db) continue;
+          if (k >= dc) continue;
           const bool age_risk = nb[k].x != s && age[k] + 2 > P.max_age;
           if (!b_trained || age_risk) {
             if (jv[k] < jj) kcn++;
@@ -502,35 +754,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             }
           }
         }
-      } else {
-        for (int k = 0; k < db; ++k) {
-          const int2 ent = B[k];
-          const int v = ent.x;
-          const bool is_s = v == s;
-          found |= is_s;
-          const int age = is_s ? 0 : S.eage[ent.y];
-          const bool age_risk = !is_s && age + 2 > P.max_age;
-          if (!b_trained || age_risk) {
-            const int jv = S.firstwin[v];
-            if (jv < jj) kcn++;
-            if (age_risk) {
-              const int a2 = jv < jj ? ((rec[jv].s == b) ? 0 : age + 1) : age;
-              if (a2 + 1 > P.max_age) ev = true;
-            }
-          }
-        }
       }
       if (!found) ev = true;  // connect_or_reset creates b-s
       const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, kcn), P.c_b) < P.h_t;
       if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
-#ifdef GS_PROF
-      atomicMax(&c->prof_max[2], clock64() - tb0);
-      atomicMax(&c->prof_lv[0], t1 - tb0);
-      atomicMax(&c->prof_lv[1], t2 - t1);
-      atomicMax(&c->prof_lv[2], t3 - t2);
-      atomicMax(&c->prof_lv[3], t4 - t3);
-      atomicMax(&c->prof_lv[4], t5 - t4);
-#endif
       int pat = -2;
       if (!ev) {
         const int ring = S.ring[b];
@@ -572,9 +799,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       s_abs[tid] = (unsigned char)((la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0));
       if (ev) evr = r;
     }
-#ifdef GS_PROF
-    if (g < nproc) atomicMax(&c->prof_max[0], clock64() - tb0);
-#endif
     const int rstar = min(cl_min(evr, s_warp, s_cta, parity), nproc);
     if (tid == 0) {
       s_i[4] = rstar < nproc ? cmap(s_plist, rstar / kUpdThreads)[rstar % kUpdThreads]
@@ -608,13 +832,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (atomicExch(&S.touchfirst[cw.b], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, cw.b);
       const int db = S.deg[cw.b];
       const int2* B = S.adj + (size_t)cw.b * kMaxDeg;
-      if (db <= kStage) {
+      for (int c0 = 0; c0 < db; c0 += kStage) {
+        const int dc = min(kStage, db - c0);
         int2 nb[kStage];
-        stage_adj(B, db, nb);
+        stage_adj(B + c0, dc, nb);
         int tf[kStage], jv[kStage], age[kStage];
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          if (k < db) {
+          if (k < dc) {
             tf[k] = atomicExch(&S.touchfirst[nb[k].x], 1);
             jv[k] = S.firstwin[nb[k].x];
             age[k] = S.eage[nb[k].y];
@@ -623,12 +848,12 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         int sv[kStage];
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          const bool mine = k < db && !(jv[k] < jstar && jv[k] > cj);
+          const bool mine = k < dc && !(jv[k] < jstar && jv[k] > cj);
           sv[k] = (mine && jv[k] < cj) ? rec[jv[k]].s : -1;
         }
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          if (k >= db) continue;
+          if (k >= dc) continue;
           if (tf[k] == kNone32) push_walk(S, s_walk, &s_nwalk, nb[k].x);
           if (jv[k] < jstar && jv[k] > cj) continue;  // v's own signal replays this edge
           int a = age[k];
@@ -636,31 +861,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           a = (nb[k].x == cw.s) ? 0 : a + 1;
           S.eage[nb[k].y] = a;
         }
-      } else {
-        for (int k = 0; k < db; ++k) {
-          const int2 ent = B[k];
-          const int v = ent.x;
-          if (atomicExch(&S.touchfirst[v], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, v);
-          const int jv = S.firstwin[v];
-          if (jv < jstar && jv > cj) continue;  // v's own signal replays this edge
-          int age = S.eage[ent.y];
-          if (jv < cj) age = (rec[jv].s == cw.b) ? 0 : age + 1;
-          age = (v == cw.s) ? 0 : age + 1;
-          S.eage[ent.y] = age;
-        }
       }
     }
     csync();
     if (lead) { const long long t_ = clock64(); c->cyc_phase[3] += t_ - t_ph; t_ph = t_; }
     // ---- C2: each touched unit's position / habituation sequence replayed once
     const int nloc = min(s_nwalk, kWalkCap);
-#ifdef GS_PROF
-    const long long tw0 = clock64();
-#endif
     for (int i = tid; i < nloc; i += kUpdThreads) walk_unit(S, P, sig, s_walk[i], jstar);
-#ifdef GS_PROF
-    if (tid < nloc) atomicMax(&c->prof_max[1], clock64() - tw0);
-#endif
     const int nglob = c->nwalk;  // overflow list (only for very high degrees)
     for (int i = g; i < nglob; i += kWinC) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
     csync();
@@ -684,74 +891,70 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       c->nwalk = 0;
       const long long t_ = clock64();
       c->cyc_phase[7] += t_ - t_ph;
-#ifdef GS_PROF
-      c->cyc_phase[4] += c->prof_max[0];
-      c->cyc_phase[5] += c->prof_max[1];
-      c->prof_max[3] += c->prof_max[2];
-      c->prof_max[0] = c->prof_max[1] = c->prof_max[2] = 0;
-      for (int q = 0; q < 5; ++q) {
-        c->prof_lvsum[q] += c->prof_lv[q];
-        c->prof_lv[q] = 0;
-      }
-#endif
       t_ph = t_;
     }
-    // ---- D: the event signal, exactly as update_single (CTA 0)
+    // ---- D: the event signal, exactly as update_single, on CTA 0: warp 0
+    //      runs the topology work lane-parallel, CTA 0's warps reclassify the
+    //      deferred rings, the lead thread finishes (sweep, adapt_threshold);
+    //      one cluster barrier publishes the result (two more only when a
+    //      sweep must scan for stale units)
     if (rstar < nproc) {
       const long long t_ser = clock64();
-      if (lead) {
-        s_defer_n = 0;
-        c->defer_n = 0;
-      }
-      __syncthreads();
-      if (crank == 0 && warp == 0) {
-        DevState SD = S;
-        SD.defer_n = &s_defer_n;
-        const WinRec r = rec[jstar];
-        const double x = sig[3 * (size_t)jstar], y = sig[3 * (size_t)jstar + 1],
-                     z = sig[3 * (size_t)jstar + 2];
-        if (lane == 0) {
-          S.claim[r.b] = batch_no;
-          event_part1a(SD, P, r.b, r.s, s_over, &s_i[3]);
-          c->processed++;
-          c->events++;
-          c->stale_n = 0;
+      if (crank == 0) {
+        if (tid == 0) s_defer_n = 0;
+        __syncthreads();
+        if (warp == 0) {
+          DevState SD = S;
+          SD.defer_n = &s_defer_n;
+          const WinRec r = rec[jstar];
+          const double x = sig[3 * (size_t)jstar], y = sig[3 * (size_t)jstar + 1],
+                       z = sig[3 * (size_t)jstar + 2];
+          if (lane == 0) {
+            S.claim[r.b] = batch_no;
+            c->processed++;
+            c->events++;
+            c->stale_n = 0;
+          }
+          w_event_part1a(SD, P, r.b, r.s, s_over, &s_i[3], s_stage);
+          // winner and neighbours move / decay: independent units, one lane each
+          if (lane == 0) {
+            double4 p = S.pos[r.b];
+            move_toward(p, P.eps_b, x, y, z);
+            S.pos[r.b] = p;
+            const double h0 = S.hab[r.b], h = dmul(h0, P.c_b);
+            S.hab[r.b] = h;
+            if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
+          }
+          const int db = S.deg[r.b];
+          const int2* B = S.adj + (size_t)r.b * kMaxDeg;
+          for (int k = lane; k < db; k += 32) {
+            const int v = B[k].x;
+            double4 p = S.pos[v];
+            move_toward(p, P.eps_n, x, y, z);
+            S.pos[v] = p;
+            const double h0 = S.hab[v], h = dmul(h0, P.c_n);
+            S.hab[v] = h;
+            if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
+          }
+          __syncwarp();
+          const long long t_mid = clock64();
+          const int fired = w_event_part1b(SD, P, r.b, r.s, r.dwin, x, y, z, s_over, s_i[3],
+                                           s_stage);
+          if (lane == 0) {
+            const long long t_end = clock64();
+            c->cyc_phase[4] += t_mid - t_ser;  // event: connect/age + moves
+            c->cyc_phase[5] += t_end - t_mid;  // event: insert + prune
+            c->ev_fired = fired;
+            c->ev_cutoff = fired ? sweep_cutoff(S, P) : 0;
+            c->ev_b = r.b;
+            c->defer_n = s_defer_n;
+          }
         }
-        __syncwarp();
-        // winner and neighbours move / decay: independent units, one lane each
-        if (lane == 0) {
-          double4 p = S.pos[r.b];
-          move_toward(p, P.eps_b, x, y, z);
-          S.pos[r.b] = p;
-          const double h0 = S.hab[r.b], h = dmul(h0, P.c_b);
-          S.hab[r.b] = h;
-          if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
-        }
-        const int db = S.deg[r.b];
-        const int2* B = S.adj + (size_t)r.b * kMaxDeg;
-        for (int k = lane; k < db; k += 32) {
-          const int v = B[k].x;
-          double4 p = S.pos[v];
-          move_toward(p, P.eps_n, x, y, z);
-          S.pos[v] = p;
-          const double h0 = S.hab[v], h = dmul(h0, P.c_n);
-          S.hab[v] = h;
-          if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
-        }
-        __syncwarp();
-        if (lane == 0) {
-          const int fired = event_part1b(SD, P, r.b, r.s, r.dwin, x, y, z, s_over, s_i[3]);
-          c->ev_fired = fired;
-          c->ev_cutoff = fired ? sweep_cutoff(S, P) : 0;
-          c->ev_b = r.b;
-          c->defer_n = s_defer_n;
-        }
-      }
-      csync();
-      // deferred ring reclassification, one warp per affected unit (cluster-wide)
-      {
-        const int nd = min(c->defer_n, kDeferCap);
-        for (int i = gwarp; i < nd; i += kCluster * (kUpdThreads / 32)) {
+        __syncthreads();
+        const long long t_rc = clock64();
+        // deferred ring reclassification, one warp per affected unit
+        const int nd = min(s_defer_n, kDeferCap);
+        for (int i = warp; i < nd; i += kUpdThreads / 32) {
           const int u = S.defer_list[i];
           if (S.alive[u]) {
             const int nw = classify_ring_warp(S, u, s_ring_sh[warp]);
@@ -766,10 +969,24 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           }
           if (lane == 0) S.touchfirst[u] = kNone32;
         }
+        __syncthreads();
+        if (tid == 0) c->cyc_phase[1] += clock64() - t_rc;  // event: ring reclassification
+        if (warp == 0 && !(c->ev_fired && c->ev_cutoff > 0)) {
+          const long long t_p2 = clock64();
+          w_event_part2(S, P, c->ev_b, c->ev_fired != 0);
+          if (lane == 0) {
+            const long long t_ = clock64();
+            c->cyc_phase[8] += t_ - t_p2;  // event: sweep clock + adapt_threshold
+            c->cyc_serial += t_ - t_ser;
+          }
+        }
       }
+      const long long t_cs = clock64();
+      csync();
+      if (lead) c->cyc_phase[9] += clock64() - t_cs;  // event: publishing barrier
       const int fired = c->ev_fired;
       const long long cutoff = c->ev_cutoff;
-      if (fired && cutoff > 0) {
+      if (fired && cutoff > 0) {  // rare: the sweep collects stale units cluster-wide
         const int nid = c->next_id;
         for (int u = g; u < nid; u += kWinC) {
           const long long t = S.la_val[u];
@@ -779,13 +996,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             S.scratch[2 * q + 1] = u;
           }
         }
+        csync();
+        if (lead) {
+          serial_update_part2(S, P, c->ev_b, c->stale_n, true);
+          c->cyc_serial += clock64() - t_ser;
+        }
+        csync();
       }
-      csync();
-      if (lead) {
-        serial_update_part2(S, P, c->ev_b, c->stale_n, fired != 0);
-        c->cyc_serial += clock64() - t_ser;
-      }
-      csync();
       j0 = jstar + 1;
     } else {
       j0 = wend;
@@ -840,14 +1057,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     st->cyc_total = c->cyc_total;
     st->batches = c->batches;
     st->halted = c->halted;
-    for (int q = 0; q < 8; ++q) st->cyc_phase[q] = c->cyc_phase[q];
-#ifdef GS_PROF
-    st->cyc_phase[1] = c->prof_max[3];  // profiling builds: B event-detection max replaces "scan"
-    st->ev_create = c->prof_lvsum[0];
-    st->ev_insert = c->prof_lvsum[1];
-    st->ev_prune = c->prof_lvsum[2];
-    st->ev_sweep = c->prof_lvsum[3];
-    st->cyc_serial = c->prof_lvsum[4];
-#endif
+    for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
   }
 }

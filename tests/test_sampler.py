@@ -14,8 +14,10 @@ from oracle.philox import PhiloxModel
 
 
 def _state_tuple(st):
+    # numpy leaves a stale uinteger behind once the pending half is used
+    has = int(st["has_uint32"])
     return (tuple(int(x) for x in st["state"]["counter"]), tuple(int(x) for x in st["buffer"]),
-            int(st["buffer_pos"]), int(st["has_uint32"]), int(st["uinteger"]))
+            int(st["buffer_pos"]), has, int(st["uinteger"]) if has else 0)
 
 
 @pytest.mark.parametrize("seed", [7, 1, 2026])
@@ -52,7 +54,7 @@ def test_device_indices_match_numpy(n_excl):
         w = s.state_words()
         st = rng.bit_generator.state
         assert (tuple(int(x) for x in w[0:4]), tuple(int(x) for x in w[6:10]), int(w[10]),
-                int(w[11]), int(w[12])) == _state_tuple(st)
+                int(w[11]), int(w[12]) if int(w[11]) else 0) == _state_tuple(st)
     s.close()
 
 

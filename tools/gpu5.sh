@@ -1,2 +1,2 @@
-GS_LIB_PATH=build_variants/lib_prof512.so timeout 300 python tools/profile_run.py cfg3
-GS_LIB_PATH=build_variants/lib_c8t512s8.so timeout 300 python tools/profile_run.py cfg3
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python tools/profile_run.py cfg3

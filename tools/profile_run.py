@@ -34,5 +34,6 @@ print(f"{name}: batches={b+1} signals={signals} V={units} conv={bool(st.converge
       f"maxdeg={st.max_degree} wall={time.perf_counter()-t0:.1f}s causes: create={st.ev_create} "
       f"insert={st.ev_insert} prune={st.ev_prune} sweep={st.ev_sweep} "
       f"serial-cycles={st.cyc_serial/max(1,st.cyc_total):.3f} of {st.cyc_total/1.9e9:.3f}s", flush=True)
-print("  window phases (s): " + " ".join(f"{n}={st.cyc_phase[i]/1.9e9:.3f}" for i, n in enumerate(
-    ("A+minla", "scan|Bdetect-max", "B", "C1", "Bmax", "walkmax", "walk", "cnt+reset"))))
+names = {0: "A+scan", 2: "B", 3: "C1", 6: "walk", 7: "reset", 4: "ev:connect+moves",
+         5: "ev:insert+prune", 1: "ev:reclass", 8: "ev:adapt", 9: "ev:barrier"}
+print("  update phases (s): " + " ".join(f"{n}={st.cyc_phase[i]/1.9e9:.3f}" for i, n in names.items()))
