@@ -161,6 +161,10 @@ struct FindArgs {
   const uint8_t* alive = nullptr;
   int64_t n = 0;                 // rows to scan (host value / upper bound)
   const int* n_dev = nullptr;    // if set: exact row count read on the device
+  // engine: row-ordered positions [3][stride] valid when *rowpos_n == rows
+  const double* rowpos = nullptr;
+  const int* rowpos_n = nullptr;
+  int64_t rowpos_stride = 0;
   const double* sig = nullptr;   // m x 3 f64
   // optional fused sampling: signal j is sig_pts[sig_idx[j]] and the find
   // writes it to sig (then non-const) for the update that follows

@@ -97,6 +97,7 @@ struct Counters {
   int stale_n;
   int converged;
   int nwalk, defer_n, ev_fired, ev_b;
+  int rowpos_n;  // rows described by rowpos (-1: stale, the find gathers through rows)
   long long ev_cutoff;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
@@ -124,6 +125,7 @@ struct DevState {
   int32_t* touchfirst;  // window scratch: owner signal per touched unit
   int32_t* iso_pos;     // index in iso_list or -1
   int32_t* rows;        // row -> id (append-only, id order)
+  double* rowpos;       // [3][U] row-ordered positions (dead rows +inf) for the find
   int32_t* eage;        // [EC]
   int32_t* efree;       // [EC] free edge-id stack
   int32_t* iso_list;    // isolated units (network.py:93 _isolated)
@@ -708,6 +710,7 @@ __device__ bool valid_unit(const DevState& S, int u) {
 
 __global__ void k_op(DevState S, Params P, OpArgs a, long long* res) {
   Counters* c = S.cnt;
+  c->rowpos_n = -1;  // positions / rows may change: the find gathers through rows
   res[0] = 0;
   res[1] = 0;
   res[2] = 0;
@@ -907,6 +910,13 @@ void grow_units(gs_engine* e, int new_u) {
   grow_array(S.touchfirst, old, new_u, st);
   grow_array(S.iso_pos, old, new_u, st);
   grow_array(S.rows, old, new_u, st);
+  if (S.rowpos) GS_CUDA(cudaFree(S.rowpos));  // regenerated by the next update (stride U)
+  GS_CUDA(cudaMalloc(&S.rowpos, sizeof(double) * 3 * (size_t)new_u));
+  {
+    const int stale = -1;
+    GS_CUDA(cudaMemcpyAsync(&S.cnt->rowpos_n, &stale, sizeof(int), cudaMemcpyHostToDevice, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+  }
   grow_array(S.iso_list, old, new_u, st);
   // scratch content is transient: plain reallocation
   if (S.scratch) GS_CUDA(cudaFree(S.scratch));
@@ -1066,6 +1076,9 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   // (n_dev) and handles past the estimate
   a.n = e->next_id;
   a.n_dev = &e->S.cnt->nrows;  // exact row count, read on the device
+  a.rowpos = e->S.rowpos;
+  a.rowpos_n = &e->S.cnt->rowpos_n;
+  a.rowpos_stride = e->U;
   a.sig = d_sig + 3 * lo;
   a.sig_idx = sig_idx ? sig_idx + lo : nullptr;
   a.sig_pts = sig_pts;
@@ -1158,7 +1171,8 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   DevState& S = e->S;
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
-                  S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res};
+                  S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
+                  S.rowpos};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (e->h_stats) cudaFreeHost(e->h_stats);

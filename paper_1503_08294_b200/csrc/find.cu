@@ -170,6 +170,7 @@ template <int kFS>
 __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, int tile_rows) {
   extern __shared__ double s_rows[];  // [3][tile_rows]
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const bool compact = a.rowpos && *a.rowpos_n == n;
   double* sx = s_rows;
   double* sy = s_rows + tile_rows;
   double* sz = s_rows + 2 * tile_rows;
@@ -208,15 +209,47 @@ __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, i
   for (int64_t t0 = 0; t0 < n; t0 += tile_rows) {
     const int nr = (int)min((int64_t)tile_rows, n - t0);
     if (t0 > 0) __syncthreads();
-    for (int r = threadIdx.x; r < nr; r += kSmallThreads) {
-      double x = kInf, y = kInf, z = kInf;
-      if (!load_row(a, t0 + r, x, y, z)) x = y = z = kInf;
-      sx[r] = x;
-      sy[r] = y;
-      sz[r] = z;
+    if (compact) {  // the update left row-ordered positions: coalesced copies
+      const double* X = a.rowpos + t0;
+      for (int r = threadIdx.x; r < nr; r += kSmallThreads) {
+        sx[r] = X[r];
+        sy[r] = X[a.rowpos_stride + r];
+        sz[r] = X[2 * a.rowpos_stride + r];
+      }
+    } else {
+      for (int r0 = 0; r0 < nr; r0 += 4 * kSmallThreads) {  // four rows in flight per thread
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = r0 + q * kSmallThreads + threadIdx.x;
+          if (r < nr) {
+            double x = kInf, y = kInf, z = kInf;
+            if (!load_row(a, t0 + r, x, y, z)) x = y = z = kInf;
+            sx[r] = x;
+            sy[r] = y;
+            sz[r] = z;
+          }
+        }
+      }
     }
     __syncthreads();
-    for (int r = slice; r < nr; r += kSmallSlices) {
+    // four rows per step: independent FP64 chains, one rarely-taken branch
+    int r = slice;
+    for (; r + 3 * kSmallSlices < nr; r += 4 * kSmallSlices) {
+#pragma unroll
+      for (int k = 0; k < kFS; ++k) {
+        double d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int rr = r + q * kSmallSlices;
+          d[q] = dist2_exact(sx[rr], sy[rr], sz[rr], qx[k], qy[k], qz[k]);
+        }
+        if (fmin(fmin(d[0], d[1]), fmin(d[2], d[3])) < b[k].d2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b[k].push(d[q], (int32_t)(t0 + r + q * kSmallSlices));
+        }
+      }
+    }
+    for (; r < nr; r += kSmallSlices) {
       const double px = sx[r], py = sy[r], pz = sz[r];
 #pragma unroll
       for (int k = 0; k < kFS; ++k)
@@ -275,6 +308,8 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
       const int bytes = 24 * kSmallMaxRows;
       GS_CUDA(cudaFuncSetAttribute(find_small_kernel<1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      GS_CUDA(cudaFuncSetAttribute(find_small_kernel<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       GS_CUDA(cudaFuncSetAttribute(find_small_kernel<4>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       attr_set = true;
@@ -283,8 +318,14 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
     const int tile_rows = (int)std::min<int64_t>(kSmallMaxRows, std::max<int64_t>(a.n, 1) + 512);
     const size_t smem = 24 * (size_t)tile_rows;
     const int64_t per1 = kSmallThreads / kSmallSlices;
-    if (a.m >= 8LL * ctx.sm_count * per1 * 4) {
+    // signals per thread: the fewest CTAs that still cover every SM once
+    // (each CTA re-stages all rows, so fewer, fuller CTAs win)
+    const int64_t sms = ctx.sm_count;
+    if (a.m >= 4 * per1 * sms) {
       find_small_kernel<4><<<(unsigned)((a.m + 4 * per1 - 1) / (4 * per1)), kSmallThreads, smem,
+                             stream>>>(a, tile_rows);
+    } else if (a.m >= 2 * per1 * sms * 2) {
+      find_small_kernel<2><<<(unsigned)((a.m + 2 * per1 - 1) / (2 * per1)), kSmallThreads, smem,
                              stream>>>(a, tile_rows);
     } else {
       find_small_kernel<1><<<(unsigned)((a.m + per1 - 1) / per1), kSmallThreads, smem, stream>>>(

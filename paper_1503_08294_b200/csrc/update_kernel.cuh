@@ -1008,9 +1008,31 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       j0 = wend;
     }
   }
+  {
+    // row-ordered positions for the next find (its staging becomes coalesced
+    // copies instead of a gather through rows); every CTA takes a slice
+    const int n = c->nrows;
+    const size_t U = (size_t)S.U;
+    for (int r0 = 0; r0 < n; r0 += 2 * kWinC) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = r0 + q * kWinC + g;
+        if (r < n) {
+          const int u = S.rows[r];
+          double4 p = make_double4(INFINITY, INFINITY, INFINITY, 0.0);
+          if (S.alive[u]) p = S.pos[u];
+          S.rowpos[r] = p.x;
+          S.rowpos[U + r] = p.y;
+          S.rowpos[2 * U + r] = p.z;
+        }
+      }
+    }
+  }
   if (crank != 0) return;
+  if (tid == 0) c->rowpos_n = c->nrows;
   // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
   if (c->ndead_rows * 8 > c->nrows) {
+    if (tid == 0) c->rowpos_n = -1;  // the rows move: the next find gathers
     const int n = c->nrows;
     int out = 0;
     for (int base = 0; base < n; base += kUpdThreads) {

@@ -27,6 +27,11 @@ for b in range(nb):
     _lib.check(lib.gs_engine_step(net.handle, batch, m, C.byref(st)))
     units = int(st.units); signals += m
     ev += st.events; win += st.windows; proc += st.processed
+    if os.environ.get("GS_FB"):
+        fb = np.zeros(2, np.int64)
+        _lib.check(lib.gs_find_last_fallback_counts(_lib.default_context().handle, fb))
+        fbs = globals().setdefault("fbs", [])
+        fbs.append(int(fb[0]))
     if st.converged:
         break
 print(f"{name}: batches={b+1} signals={signals} V={units} conv={bool(st.converged)} "
@@ -34,6 +39,9 @@ print(f"{name}: batches={b+1} signals={signals} V={units} conv={bool(st.converge
       f"maxdeg={st.max_degree} wall={time.perf_counter()-t0:.1f}s causes: create={st.ev_create} "
       f"insert={st.ev_insert} prune={st.ev_prune} sweep={st.ev_sweep} "
       f"serial-cycles={st.cyc_serial/max(1,st.cyc_total):.3f} of {st.cyc_total/1.9e9:.3f}s", flush=True)
+if os.environ.get("GS_FB"):
+    print("find fallbacks per batch: mean %.1f, last-100 mean %.1f, max %d" % (
+        np.mean(fbs), np.mean(fbs[-100:]), max(fbs)))
 names = {0: "A+scan", 2: "B", 3: "C1", 6: "walk", 7: "reset", 4: "ev:connect+moves",
          5: "ev:insert+prune", 1: "ev:reclass", 8: "ev:adapt", 9: "ev:barrier"}
 print("  update phases (s): " + " ".join(f"{n}={st.cyc_phase[i]/1.9e9:.3f}" for i, n in names.items()))
