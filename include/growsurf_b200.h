@@ -190,7 +190,10 @@ gs_status gs_engine_stats(gs_engine *eng, gs_batch_stats *out);
 void *gs_engine_stream(gs_engine *eng);
 /* Allow up to `depth` batches to be enqueued ahead of the host's stats reads:
  * once converged, later batches leave the network untouched (stats.halted),
- * and stats.batches counts the batches that ran.  0 = synchronous contract. */
+ * and stats.batches counts the batches that ran.  0 = synchronous contract.
+ * While async, gs_engine_step_sampled draws `depth` batches of indices per
+ * sampler launch (the batch size must stay fixed), so the sampler's state
+ * may run up to depth-1 batches ahead of the batches executed. */
 gs_status gs_engine_set_async(gs_engine *eng, int depth);
 /* Pre-size device storage for ids [0, n) (avoids growth inside timed loops). */
 gs_status gs_engine_reserve(gs_engine *eng, int64_t n);

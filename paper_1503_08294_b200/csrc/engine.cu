@@ -862,6 +862,9 @@ struct gs_engine {
   int next_id = 0, n_edges = 0, n_units = 0;
   // batches the host may enqueue ahead of its last stats read (gs_engine_set_async)
   int async_depth = 0;
+  // asynchronous sampled runs draw the indices of async_depth batches per
+  // sampler launch (fixed batch size)
+  int64_t pf_m = 0, pf_next = 0, pf_left = 0;
 };
 
 namespace {
@@ -1371,9 +1374,30 @@ extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64
   return guarded([&] {
     GS_CHECK(e && smp && m > 0, GS_VALUE_ERROR, "bad step arguments");
     double* d_sig = (double*)e->sig_buf.get(sizeof(double) * 3 * (size_t)m);
-    int64_t* d_idx = (int64_t*)e->idx_buf.get(sizeof(int64_t) * (size_t)m);
-    sampler_indices(smp, m, d_idx, e->stream);
-    e->launches++;
+    int64_t* d_idx;
+    if (e->async_depth > 0) {
+      // one sampler launch draws the next async_depth batches (same stream
+      // order as one launch per batch); a batch-size change would reorder
+      // draws already taken, so it is an error while some remain
+      GS_CHECK(e->pf_left == 0 || e->pf_m == m, GS_VALUE_ERROR,
+               "asynchronous sampled runs need a fixed batch size");
+      if (e->pf_left == 0) {
+        const int64_t k = e->async_depth;
+        int64_t* ring = (int64_t*)e->idx_buf.get(sizeof(int64_t) * (size_t)(k * m));
+        sampler_indices(smp, k * m, ring, e->stream);
+        e->launches++;
+        e->pf_m = m;
+        e->pf_next = 0;
+        e->pf_left = k;
+      }
+      d_idx = (int64_t*)e->idx_buf.p + e->pf_next * m;
+      e->pf_next++;
+      e->pf_left--;
+    } else {
+      d_idx = (int64_t*)e->idx_buf.get(sizeof(int64_t) * (size_t)m);
+      sampler_indices(smp, m, d_idx, e->stream);
+      e->launches++;
+    }
     step_device_impl(e, d_sig, m, d_idx, sampler_points(smp));
     if (out) {
       GS_CUDA(cudaStreamSynchronize(e->stream));
@@ -1476,6 +1500,7 @@ extern "C" gs_status gs_engine_set_async(gs_engine* e, int depth) {
   return guarded([&] {
     GS_CHECK(e && depth >= 0 && depth <= 1024, GS_VALUE_ERROR, "bad async depth");
     e->async_depth = depth;
+    e->pf_left = e->pf_next = 0;  // prefetched indices (if any) are dropped
     // {halt_on_converge, halted}: leaving async mode also clears the halt, so
     // the network can be stepped further like the reference's
     const int flags[2] = {depth > 0 ? 1 : 0, 0};
@@ -1509,6 +1534,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     GS_CUDA(cudaMemsetAsync(S.stats, 0, sizeof(gs_batch_stats), st));
     GS_CUDA(cudaStreamSynchronize(st));
     e->next_id = e->n_edges = e->n_units = 0;
+    e->pf_left = e->pf_next = 0;
     memset(e->h_stats, 0, sizeof(gs_batch_stats));
     e->find_ms = e->update_ms = 0.0;
     e->ev_pending = false;
