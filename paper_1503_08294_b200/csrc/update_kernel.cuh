@@ -719,6 +719,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       const double hbT = S.hab[b];
       const double thb = S.theta[b];
       const long long la_b = S.la_val[b], la_s = S.la_val[s];
+      const int ringb = S.ring[b], patb = S.patience[b];
       const bool b_trained = hbT < P.h_t;
       bool found = false;
       int kcn = 0;
@@ -760,34 +761,53 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
       int pat = -2;
       if (!ev) {
-        const int ring = S.ring[b];
-        if (ring == kRingDisk || (P.allow_boundary && ring == kRingHalf)) {
+        if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) {
           pat = 0;
         } else if (hb_low) {
+          // every neighbour must be trained at time jj (engine.py:225-231):
+          // neighbours' habituation loads issue together per chunk; only the
+          // untrained-at-window-start ones need their decays replayed
           bool ok = true;
-          for (int k = 0; k < db && ok; ++k) {
-            const int v = B[k].x;
-            const double hvT = S.hab[v];
-            if (hvT < P.h_t) continue;
-            const int jv = S.firstwin[v];
-            const bool vwon = jv < jj;
-            const int dv = S.deg[v];
-            const int2* V = S.adj + (size_t)v * kMaxDeg;
-            int k1 = 0, k2 = 0;
-            for (int q = 0; q < dv; ++q) {
-              const int jw = S.firstwin[V[q].x];
-              if (jw <= jj) {
-                if (vwon && jw > jv) k2++;
-                else k1++;
+          for (int c0 = 0; c0 < db && ok; c0 += kStage) {
+            const int dc = min(kStage, db - c0);
+            int2 nb[kStage];
+            stage_adj(B + c0, dc, nb);
+            double hv0[kStage];
+#pragma unroll
+            for (int k = 0; k < kStage; ++k) hv0[k] = k < dc ? S.hab[nb[k].x] : 0.0;
+#pragma unroll 1
+            for (int k = 0; k < dc && ok; ++k) {
+              const double hvT = hv0[k];
+              if (hvT < P.h_t) continue;
+              const int v = nb[k].x;
+              const int jv = S.firstwin[v];
+              const bool vwon = jv < jj;
+              const int dv = S.deg[v];
+              const int2* V = S.adj + (size_t)v * kMaxDeg;
+              int k1 = 0, k2 = 0;
+              for (int q0 = 0; q0 < dv; q0 += kStage) {
+                const int dq = min(kStage, dv - q0);
+                int2 wb[kStage];
+                stage_adj(V + q0, dq, wb);
+                int jw[kStage];
+#pragma unroll
+                for (int q = 0; q < kStage; ++q) jw[q] = q < dq ? S.firstwin[wb[q].x] : kNone32;
+#pragma unroll
+                for (int q = 0; q < kStage; ++q) {
+                  if (q < dq && jw[q] <= jj) {
+                    if (vwon && jw[q] > jv) k2++;
+                    else k1++;
+                  }
+                }
               }
+              double hv = pow_chain(hvT, P.c_n, k1);
+              if (vwon) hv = dmul(hv, P.c_b);
+              hv = pow_chain(hv, P.c_n, k2);
+              if (hv >= P.h_t) ok = false;
             }
-            double hv = pow_chain(hvT, P.c_n, k1);
-            if (vwon) hv = dmul(hv, P.c_b);
-            hv = pow_chain(hv, P.c_n, k2);
-            if (hv >= P.h_t) ok = false;
           }
           if (ok) {
-            int cnt = S.patience[b] + 1;
+            int cnt = patb + 1;
             const int shrink = cnt >= P.ring_patience ? 1 : 0;
             if (shrink) cnt = 0;
             pat = cnt | (shrink << 30);

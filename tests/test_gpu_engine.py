@@ -250,3 +250,22 @@ def test_cfg3_headline_run_matches_reference():
         assert np.array_equal(got[k].view(np.int64), gold[k].view(np.int64)), k
     mesh = extract_mesh(net)
     assert manifold_check(mesh) == "closed" and genus(mesh) == 2
+
+
+@pytest.mark.parametrize("name", ["paper_rule", "boundary", "cfg1"])
+def test_run_multi_device_sampling_matches_golden(name):
+    """run_multi on a CloudSource draws its batches on the device (variable m
+    under the paper's batch rule: synchronous; fixed m: the asynchronous
+    lookahead loop) and must reproduce the reference's run bit for bit."""
+    from paper_1503_08294_b200 import EngineParams, run_multi
+
+    gold = load_golden(name)
+    if not same_numpy(gold):
+        pytest.skip("golden made with another numpy")
+    case = CASES[name]
+    params = EngineParams(**case["params"])
+    net, st = run_multi(make_source(case["source"]), params, case["seed"])
+    for k in ("iterations", "signals", "discarded", "units", "connections", "converged"):
+        assert int(getattr(st, k)) == int(gold[f"stat_{k}"]), k
+    assert_state_equal(net.export(), gold)
+    net.audit()
