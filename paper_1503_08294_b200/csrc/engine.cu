@@ -98,6 +98,7 @@ struct Counters {
   int converged;
   int nwalk, defer_n, ev_fired, ev_b;
   int rowpos_n;  // rows described by rowpos (-1: stale, the find gathers through rows)
+  int deaths;    // units removed so far (an event without deaths lets the window resume)
   long long ev_cutoff;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
@@ -333,6 +334,7 @@ __device__ void remove_unit_raw(const DevState& S, const Params& P, int u) {
   iso_del(S, u);
   if (S.hab[u] >= P.h_t) c->untrained--;
   c->ndead_rows++;
+  c->deaths++;
 }
 
 // remove_unit: network.py:232-240
@@ -854,9 +856,13 @@ struct gs_engine {
   long long* h_res = nullptr;
   int batch_no = 0;
   long long launches = 0;
-  // optional per-phase device timing (CUDA events on the engine stream)
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  bool timing = false, ev_pending = false;
+  // optional per-phase device timing: a ring of (start, find done, update
+  // done) CUDA events on the engine stream, so every batch is timed even
+  // with batches in flight; harvested at the next synchronisation
+  static constexpr int kEvRing = 64;
+  cudaEvent_t ev[kEvRing][3] = {};
+  int ev_head = 0, ev_count = 0;
+  bool timing = false;
   double find_ms = 0.0, update_ms = 0.0;
   // host mirror of the last known counters
   int next_id = 0, n_edges = 0, n_units = 0;
@@ -1181,8 +1187,9 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   if (e->h_stats) cudaFreeHost(e->h_stats);
   if (e->h_res) cudaFreeHost(e->h_res);
   if (e->h_sig) cudaFreeHost(e->h_sig);
-  for (auto ev : e->ev)
-    if (ev) cudaEventDestroy(ev);
+  for (auto& trio : e->ev)
+    for (auto ev : trio)
+      if (ev) cudaEventDestroy(ev);
   e->find_work.release();
   e->sig_buf.release();
   e->rec_buf.release();
@@ -1300,6 +1307,8 @@ extern "C" gs_status gs_engine_set_unit(gs_engine* e, int64_t id, const double* 
 }
 
 namespace {
+void harvest_timing(gs_engine* e);
+
 // find + update for one batch on the engine stream.  With sig_idx the find
 // gathers the signals from the sampler's cloud into d_sig (fused sampling).
 void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_t* sig_idx,
@@ -1308,14 +1317,16 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
   ensure_capacity(e, m, 3 * m);
   WinRec* rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
-  const bool timed = e->timing && !e->ev_pending;
-  if (timed) GS_CUDA(cudaEventRecord(e->ev[0], e->stream));
+  if (e->timing && e->ev_count == gs_engine::kEvRing) harvest_timing(e);  // ring full: sync
+  const bool timed = e->timing;
+  cudaEvent_t* evs = e->ev[(e->ev_head + e->ev_count) % gs_engine::kEvRing];
+  if (timed) GS_CUDA(cudaEventRecord(evs[0], e->stream));
   launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
-  if (timed) GS_CUDA(cudaEventRecord(e->ev[1], e->stream));
+  if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
   launch_update(e, d_sig, rec, m);
   if (timed) {
-    GS_CUDA(cudaEventRecord(e->ev[2], e->stream));
-    e->ev_pending = true;
+    GS_CUDA(cudaEventRecord(evs[2], e->stream));
+    e->ev_count++;
   }
   GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
                           cudaMemcpyDeviceToHost, e->stream));
@@ -1328,21 +1339,25 @@ extern "C" gs_status gs_engine_step_device(gs_engine* e, const double* d_sig, in
 
 namespace {
 void harvest_timing(gs_engine* e) {
-  if (!e->ev_pending) return;
-  float a = 0.f, b = 0.f;
-  GS_CUDA(cudaEventElapsedTime(&a, e->ev[0], e->ev[1]));
-  GS_CUDA(cudaEventElapsedTime(&b, e->ev[1], e->ev[2]));
-  e->find_ms += a;
-  e->update_ms += b;
-  e->ev_pending = false;
+  for (; e->ev_count > 0; --e->ev_count) {
+    cudaEvent_t* evs = e->ev[e->ev_head];
+    float a = 0.f, b = 0.f;
+    GS_CUDA(cudaEventSynchronize(evs[2]));
+    GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
+    GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
+    e->find_ms += a;
+    e->update_ms += b;
+    e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
+  }
 }
 }  // namespace
 
 extern "C" gs_status gs_engine_phase_ms(gs_engine* e, int enable, double out[2]) {
   return guarded([&] {
     GS_CHECK(e, GS_VALUE_ERROR, "null engine");
-    if (enable >= 0 && !e->ev[0]) {
-      for (auto& ev : e->ev) GS_CUDA(cudaEventCreate(&ev));
+    if (enable >= 0 && !e->ev[0][0]) {
+      for (auto& trio : e->ev)
+        for (auto& ev : trio) GS_CUDA(cudaEventCreate(&ev));
     }
     if (enable >= 0) e->timing = enable != 0;
     if (out) {
@@ -1536,8 +1551,8 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     e->next_id = e->n_edges = e->n_units = 0;
     e->pf_left = e->pf_next = 0;
     memset(e->h_stats, 0, sizeof(gs_batch_stats));
+    harvest_timing(e);
     e->find_ms = e->update_ms = 0.0;
-    e->ev_pending = false;
   });
 }
 

@@ -646,7 +646,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const int g = crank * kUpdThreads + tid;  // cluster-wide thread index
   const bool lead = crank == 0 && tid == 0;
   const int warp = tid >> 5, lane = tid & 31;
-  const int gwarp = crank * (kUpdThreads / 32) + warp;
   int parity = 0;
   if (S.cnt->halted) return;  // converged earlier in an asynchronous run (uniform)
   const long long t_kernel = clock64();
@@ -660,48 +659,63 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   if (tid == 0) s_nwalk = 0;
   csync();
   int j0 = 0;
+  // A window [j0, wend) is evaluated once (A: candidates, scan: processed
+  // list by rank) and committed in segments of ranks [rbase, r*): after an
+  // event that removed no unit the candidate set and ranks are unchanged, so
+  // the window RESUMES at rank r*+1 (B re-evaluates the remaining ranks
+  // against the post-event state); an event with deaths closes the window
+  // and the next one starts at j*+1.
+  bool resume = false;
+  int rbase = 0, nproc = 0, wend = 0;
+  long long tick0 = 0, minla = 0;
+  bool cand = false;
+  int cb = -1;
   while (j0 < m) {
     if (lead) t_ph = clock64();
-    const int wend = min(j0 + kWinC, m);
-    const int next_id = c->next_id;
-    const long long tick0 = c->tick;
+    if (!resume) {
+      wend = min(j0 + kWinC, m);
+      const int next_id = c->next_id;
+      tick0 = c->tick;
+      const long long next_sweep0 = c->next_sweep;
+      // ---- A: candidates; the first candidate per winner is processed
+      const int j = j0 + g;
+      cand = false;
+      cb = -1;
+      if (j < wend) {
+        const WinRec r = rec[j];
+        cb = r.b;
+        cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
+               S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
+        if (cand) atomicMin(&S.firstwin[r.b], j);
+      }
+      // minimum last_active over live units (silent-sweep test), window start;
+      // it only grows, so later segments may use this (conservative) value
+      long long mla = 0x7fffffffffffffffLL;
+      if (tick0 + kWinC >= next_sweep0) {
+        for (int u = g; u < next_id; u += kWinC) {
+          const long long t = S.la_val[u];
+          if (t != -1 && S.alive[u] && t < mla) mla = t;
+        }
+      }
+      minla = cl_min_ll(mla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
+      if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
+      const bool proc = cand && S.firstwin[cb] == j;
+      const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
+      if (proc) {
+        int* dst = cmap(s_plist, rank / kUpdThreads);
+        dst[rank % kUpdThreads] = j;
+      }
+      csync();
+      rbase = 0;
+      if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
+    }
     const long long next_sweep = c->next_sweep;
     const int n_units = c->n_units;
     const bool iso = c->iso_count > 0;
-    // ---- A: candidates; the first candidate per winner is processed
-    const int j = j0 + g;
-    bool cand = false;
-    int cb = -1;
-    if (j < wend) {
-      const WinRec r = rec[j];
-      cb = r.b;
-      cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
-             S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
-      if (cand) atomicMin(&S.firstwin[r.b], j);
-    }
-    // minimum last_active over live units (silent-sweep test), window start
-    long long minla = 0x7fffffffffffffffLL;
-    if (tick0 + kWinC >= next_sweep) {
-      for (int u = g; u < next_id; u += kWinC) {
-        const long long t = S.la_val[u];
-        if (t != -1 && S.alive[u] && t < minla) minla = t;
-      }
-    }
-    minla = cl_min_ll(minla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
-    const bool proc = cand && S.firstwin[cb] == j;
-    int nproc;
-    const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
-    if (proc) {
-      int* dst = cmap(s_plist, rank / kUpdThreads);
-      dst[rank % kUpdThreads] = j;
-    }
-    csync();
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
     // ---- B: events and adapt_threshold outcomes; thread g owns rank g
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     int evr = 0x7fffffff;
-    if (g < nproc) {
+    if (g >= rbase && g < nproc) {
       const int r = g;
       const int jj = s_plist[tid];
       const WinRec w = rec[jj];
@@ -829,7 +843,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     if (lead) { const long long t_ = clock64(); c->cyc_phase[2] += t_ - t_ph; t_ph = t_; }
     // ---- C1: claims, last_active (+ order stamps), patience/threshold,
     //      touched-unit owners, edge-age replay
-    const bool com = g < rstar;
+    const bool com = g >= rbase && g < rstar;
     WinRec cw;
     int cj = 0;
     if (com) {
@@ -893,16 +907,19 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     csync();
     if (lead) { const long long t_ = clock64(); c->cyc_phase[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
+    // the window closes here unless an event without deaths lets it resume
+    // (decided after the event; a closing window clears every candidate's
+    // firstwin, a resuming one only the committed winners')
     if (lead) {
       c->tick = tick0 + rstar;
-      c->processed += rstar;
-      c->discarded += (jstar - j0) - rstar;
+      c->processed += rstar - rbase;
       c->windows++;
       long long ns = next_sweep;  // silent sweeps among the committed ticks
       while (ns <= tick0 + rstar) ns += kSweepEvery;
       c->next_sweep = ns;
     }
-    if (cand) S.firstwin[cb] = kNone32;
+    if (com) S.firstwin[cw.b] = kNone32;
+    const int deaths0 = c->deaths;  // stable until the event path (read before its barrier)
     for (int i = tid; i < nloc; i += kUpdThreads) S.touchfirst[s_walk[i]] = kNone32;
     for (int i = g; i < nglob; i += kWinC) S.touchfirst[(int)S.scratch[i]] = kNone32;
     csync();
@@ -931,6 +948,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
                        z = sig[3 * (size_t)jstar + 2];
           if (lane == 0) {
             S.claim[r.b] = batch_no;
+            S.firstwin[r.b] = kNone32;  // committed: later segments must not replay it
             c->processed++;
             c->events++;
             c->stale_n = 0;
@@ -1023,10 +1041,22 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         }
         csync();
       }
-      j0 = jstar + 1;
+      // resume the window after an event that removed no unit
+      resume = c->deaths == deaths0 && rstar + 1 < nproc;
+      if (resume) {
+        rbase = rstar + 1;
+      } else {
+        if (lead) c->discarded += (jstar + 1 - j0) - (rstar + 1);
+        if (cand) S.firstwin[cb] = kNone32;
+        j0 = jstar + 1;
+      }
     } else {
+      if (lead) c->discarded += (wend - j0) - nproc;
+      if (cand) S.firstwin[cb] = kNone32;
+      resume = false;
       j0 = wend;
     }
+    if (!resume) csync();  // firstwin cleared before the next window's candidates
   }
   {
     // row-ordered positions for the next find (its staging becomes coalesced
