@@ -650,6 +650,11 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   if (S.cnt->halted) return;  // converged earlier in an asynchronous run (uniform)
   const long long t_kernel = clock64();
   long long t_ph = t_kernel;
+  // the lead thread's phase timers stay in registers until the kernel ends
+  // (a global read-modify-write per phase would sit on its critical path)
+  long long acc[13];
+#pragma unroll
+  for (int q = 0; q < 13; ++q) acc[q] = 0;
   if (lead) {
     c->processed = c->discarded = c->events = c->windows = 0;
     c->inserted_start = c->next_id;
@@ -698,7 +703,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         }
       }
       minla = cl_min_ll(mla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
-      if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
+      if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
       const bool proc = cand && S.firstwin[cb] == j;
       const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
       if (proc) {
@@ -707,7 +712,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       }
       csync();
       rbase = 0;
-      if (lead) { const long long t_ = clock64(); c->cyc_phase[0] += t_ - t_ph; t_ph = t_; }
+      if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
     }
     const long long next_sweep = c->next_sweep;
     const int n_units = c->n_units;
@@ -840,7 +845,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
     __syncthreads();
     const int jstar = s_i[4];
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[2] += t_ - t_ph; t_ph = t_; }
+    if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
     // ---- C1: claims, last_active (+ order stamps), patience/threshold,
     //      touched-unit owners, edge-age replay
     const bool com = g >= rbase && g < rstar;
@@ -898,14 +903,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       }
     }
     csync();
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[3] += t_ - t_ph; t_ph = t_; }
+    if (lead) { const long long t_ = clock64(); acc[3] += t_ - t_ph; t_ph = t_; }
     // ---- C2: each touched unit's position / habituation sequence replayed once
     const int nloc = min(s_nwalk, kWalkCap);
     for (int i = tid; i < nloc; i += kUpdThreads) walk_unit(S, P, sig, s_walk[i], jstar);
     const int nglob = c->nwalk;  // overflow list (only for very high degrees)
     for (int i = g; i < nglob; i += kWinC) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
     csync();
-    if (lead) { const long long t_ = clock64(); c->cyc_phase[6] += t_ - t_ph; t_ph = t_; }
+    if (lead) { const long long t_ = clock64(); acc[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
     // the window closes here unless an event without deaths lets it resume
     // (decided after the event; a closing window clears every candidate's
@@ -927,7 +932,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     if (lead) {
       c->nwalk = 0;
       const long long t_ = clock64();
-      c->cyc_phase[7] += t_ - t_ph;
+      acc[7] += t_ - t_ph;
       t_ph = t_;
     }
     // ---- D: the event signal, exactly as update_single, on CTA 0: warp 0
@@ -980,8 +985,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
                                            s_stage);
           if (lane == 0) {
             const long long t_end = clock64();
-            c->cyc_phase[4] += t_mid - t_ser;  // event: connect/age + moves
-            c->cyc_phase[5] += t_end - t_mid;  // event: insert + prune
+            acc[4] += t_mid - t_ser;  // event: connect/age + moves
+            acc[5] += t_end - t_mid;  // event: insert + prune
             c->ev_fired = fired;
             c->ev_cutoff = fired ? sweep_cutoff(S, P) : 0;
             c->ev_b = r.b;
@@ -1008,20 +1013,20 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           if (lane == 0) S.touchfirst[u] = kNone32;
         }
         __syncthreads();
-        if (tid == 0) c->cyc_phase[1] += clock64() - t_rc;  // event: ring reclassification
+        if (tid == 0) acc[1] += clock64() - t_rc;  // event: ring reclassification
         if (warp == 0 && !(c->ev_fired && c->ev_cutoff > 0)) {
           const long long t_p2 = clock64();
           w_event_part2(S, P, c->ev_b, c->ev_fired != 0);
           if (lane == 0) {
             const long long t_ = clock64();
-            c->cyc_phase[8] += t_ - t_p2;  // event: sweep clock + adapt_threshold
-            c->cyc_serial += t_ - t_ser;
+            acc[8] += t_ - t_p2;  // event: sweep clock + adapt_threshold
+            acc[12] += t_ - t_ser;
           }
         }
       }
       const long long t_cs = clock64();
       csync();
-      if (lead) c->cyc_phase[9] += clock64() - t_cs;  // event: publishing barrier
+      if (lead) acc[9] += clock64() - t_cs;  // event: publishing barrier
       const int fired = c->ev_fired;
       const long long cutoff = c->ev_cutoff;
       if (fired && cutoff > 0) {  // rare: the sweep collects stale units cluster-wide
@@ -1037,7 +1042,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         csync();
         if (lead) {
           serial_update_part2(S, P, c->ev_b, c->stale_n, true);
-          c->cyc_serial += clock64() - t_ser;
+          acc[12] += clock64() - t_ser;
         }
         csync();
       }
@@ -1125,6 +1130,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     st->ev_prune = c->ev_prune;
     st->ev_sweep = c->ev_sweep;
     c->cyc_total += clock64() - t_kernel;
+#pragma unroll
+    for (int q = 0; q < 12; ++q) c->cyc_phase[q] += acc[q];
+    c->cyc_serial += acc[12];
     st->cyc_serial = c->cyc_serial;
     st->cyc_total = c->cyc_total;
     st->batches = c->batches;
