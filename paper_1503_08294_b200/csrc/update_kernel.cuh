@@ -640,6 +640,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
   __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
+  __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
   Counters* c = S.cnt;
   const int tid = threadIdx.x;
   const int crank = crank_of();
@@ -946,17 +947,29 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         if (tid == 0) s_defer_n = 0;
         __syncthreads();
         if (warp == 0) {
+          // the event's counter traffic (tick, free-edge stack, unit / edge /
+          // ring counts, isolated list length...) runs on a shared-memory copy
+          // of the counters: warp 0 is the only user until the copy-back
+          constexpr int kCntWords = (int)(sizeof(Counters) / sizeof(int));
+          {
+            const int* src = reinterpret_cast<const int*>(c);
+            int* dst = reinterpret_cast<int*>(&s_cnt);
+            for (int q = lane; q < kCntWords; q += 32) dst[q] = src[q];
+          }
+          __syncwarp();
+          Counters* cc = &s_cnt;
           DevState SD = S;
           SD.defer_n = &s_defer_n;
+          SD.cnt = cc;
           const WinRec r = rec[jstar];
           const double x = sig[3 * (size_t)jstar], y = sig[3 * (size_t)jstar + 1],
                        z = sig[3 * (size_t)jstar + 2];
           if (lane == 0) {
             S.claim[r.b] = batch_no;
             S.firstwin[r.b] = kNone32;  // committed: later segments must not replay it
-            c->processed++;
-            c->events++;
-            c->stale_n = 0;
+            cc->processed++;
+            cc->events++;
+            cc->stale_n = 0;
           }
           w_event_part1a(SD, P, r.b, r.s, s_over, &s_i[3], s_stage);
           // winner and neighbours move / decay: independent units, one lane each
@@ -966,7 +979,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             S.pos[r.b] = p;
             const double h0 = S.hab[r.b], h = dmul(h0, P.c_b);
             S.hab[r.b] = h;
-            if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
+            if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
           }
           const int db = S.deg[r.b];
           const int2* B = S.adj + (size_t)r.b * kMaxDeg;
@@ -977,7 +990,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             S.pos[v] = p;
             const double h0 = S.hab[v], h = dmul(h0, P.c_n);
             S.hab[v] = h;
-            if (h0 >= P.h_t && h < P.h_t) atomicSub(&c->untrained, 1);
+            if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
           }
           __syncwarp();
           const long long t_mid = clock64();
@@ -987,10 +1000,16 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             const long long t_end = clock64();
             acc[4] += t_mid - t_ser;  // event: connect/age + moves
             acc[5] += t_end - t_mid;  // event: insert + prune
-            c->ev_fired = fired;
-            c->ev_cutoff = fired ? sweep_cutoff(S, P) : 0;
-            c->ev_b = r.b;
-            c->defer_n = s_defer_n;
+            cc->ev_fired = fired;
+            cc->ev_cutoff = fired ? sweep_cutoff(SD, P) : 0;
+            cc->ev_b = r.b;
+            cc->defer_n = s_defer_n;
+          }
+          __syncwarp();
+          {
+            const int* src = reinterpret_cast<const int*>(&s_cnt);
+            int* dst = reinterpret_cast<int*>(c);
+            for (int q = lane; q < kCntWords; q += 32) dst[q] = src[q];
           }
         }
         __syncthreads();
