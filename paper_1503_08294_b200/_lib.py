@@ -84,6 +84,8 @@ _SIGNATURES = {
     "gs_engine_set_params": (C.c_int, [_vp, C.POINTER(GsParams)]),
     "gs_engine_phase_ms": (C.c_int, [_vp, C.c_int, _f64p]),
     "gs_engine_stats": (C.c_int, [_vp, C.POINTER(GsBatchStats)]),
+    "gs_engine_stats_lagged": (C.c_int, [_vp, C.c_int64, C.POINTER(GsBatchStats),
+                                         C.POINTER(C.c_int64)]),
     "gs_engine_stream": (_vp, [_vp]),
     "gs_engine_reserve": (C.c_int, [_vp, C.c_int64]),
     "gs_engine_launch_count": (C.c_int64, [_vp]),

@@ -850,6 +850,13 @@ struct gs_engine {
   DevBuf rec_buf;
   DevBuf idx_buf;  // sampled cloud indices (gs_engine_step_sampled)
   gs_batch_stats* h_stats = nullptr;  // pinned
+  // per-batch stats copies (ring of pinned slots + completion events) so the
+  // host can read batch i - lag while later batches are still queued
+  gs_batch_stats* h_ring = nullptr;
+  cudaEvent_t stat_ev[64] = {};
+  int64_t issued = 0;
+  int64_t reset_seq = 0;     // steps issued before the last reset (stale for lagged reads)
+  bool ring_latest = false;  // h_ring holds the newest stats (device steps)
   double* h_sig = nullptr;            // pinned staging for host batches
   size_t h_sig_cap = 0;
   long long* d_res = nullptr;
@@ -1159,6 +1166,9 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
       GS_CUDA(cudaMalloc(&e->S.defer_list, sizeof(int32_t) * kDeferCap));
       GS_CUDA(cudaMallocHost(&e->h_stats, sizeof(gs_batch_stats)));
       memset(e->h_stats, 0, sizeof(gs_batch_stats));
+      GS_CUDA(cudaMallocHost(&e->h_ring, sizeof(gs_batch_stats) * gs_engine::kEvRing));
+      memset(e->h_ring, 0, sizeof(gs_batch_stats) * gs_engine::kEvRing);
+      for (auto& ev : e->stat_ev) GS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       GS_CUDA(cudaMalloc(&e->d_res, 4 * sizeof(long long)));
       GS_CUDA(cudaMallocHost(&e->h_res, 4 * sizeof(long long)));
       const int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(capacity_hint, 1 << 28));
@@ -1185,6 +1195,9 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (e->h_stats) cudaFreeHost(e->h_stats);
+  if (e->h_ring) cudaFreeHost(e->h_ring);
+  for (auto ev : e->stat_ev)
+    if (ev) cudaEventDestroy(ev);
   if (e->h_res) cudaFreeHost(e->h_res);
   if (e->h_sig) cudaFreeHost(e->h_sig);
   for (auto& trio : e->ev)
@@ -1328,8 +1341,12 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;
   }
-  GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
+  const int slot = (int)(e->issued % gs_engine::kEvRing);
+  GS_CUDA(cudaMemcpyAsync(e->h_ring + slot, e->S.stats, sizeof(gs_batch_stats),
                           cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
+  e->issued++;
+  e->ring_latest = true;
 }
 }  // namespace
 
@@ -1367,19 +1384,55 @@ extern "C" gs_status gs_engine_phase_ms(gs_engine* e, int enable, double out[2])
   });
 }
 
+// newest device-step stats into h_stats (after the stream is idle)
+void latest_stats(gs_engine* e) {
+  if (e->ring_latest && e->issued > 0)
+    *e->h_stats = e->h_ring[(e->issued - 1) % gs_engine::kEvRing];
+}
+
 extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
   return guarded([&] {
     GS_CHECK(e, GS_VALUE_ERROR, "null engine");
     GS_CUDA(cudaStreamSynchronize(e->stream));
+    latest_stats(e);
     harvest_timing(e);
     check_stats(e);
     if (out) *out = *e->h_stats;
   });
 }
 
-// One iteration whose m signals are drawn on the device by a CloudSource
-// sampler (sample.cu) into the engine's signal buffer; out != NULL makes it
-// synchronous (stats copied out), else it stays queued on the engine stream.
+// Stats of the batch issued `lag` batches before the newest, waiting only for
+// that batch (later ones keep the GPU busy).  *seq receives its index among
+// the device steps issued so far (-1: fewer than lag + 1 issued; out zeroed).
+extern "C" gs_status gs_engine_stats_lagged(gs_engine* e, int64_t lag, gs_batch_stats* out,
+                                            int64_t* seq) {
+  return guarded([&] {
+    GS_CHECK(e && out && lag >= 0 && lag < gs_engine::kEvRing - 1, GS_VALUE_ERROR,
+             "lag must be in [0, 63)");
+    const int64_t target = e->issued - 1 - lag;
+    if (seq) *seq = target < e->reset_seq ? -1 : target - e->reset_seq;
+    if (target < e->reset_seq) {
+      memset(out, 0, sizeof(*out));
+      return;
+    }
+    GS_CUDA(cudaEventSynchronize(e->stat_ev[target % gs_engine::kEvRing]));
+    // per-phase timings of the batches known complete
+    while (e->ev_count > 0 && (int64_t)e->ev_count > lag) {
+      cudaEvent_t* evs = e->ev[e->ev_head];
+      float a = 0.f, b = 0.f;
+      GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
+      GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
+      e->find_ms += a;
+      e->update_ms += b;
+      e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
+      e->ev_count--;
+    }
+    *e->h_stats = e->h_ring[target % gs_engine::kEvRing];
+    check_stats(e);
+    *out = *e->h_stats;
+  });
+}
+
 // One iteration whose m signals are drawn on the device by a CloudSource
 // sampler (sample.cu): the sampler kernel emits cloud indices, the find
 // gathers the points into the engine's signal buffer as it loads them.
@@ -1416,6 +1469,7 @@ extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64
     step_device_impl(e, d_sig, m, d_idx, sampler_points(smp));
     if (out) {
       GS_CUDA(cudaStreamSynchronize(e->stream));
+      latest_stats(e);
       harvest_timing(e);
       check_stats(e);
       *out = *e->h_stats;
@@ -1439,6 +1493,7 @@ extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t
     gs_status st = gs_engine_step_device(e, d_sig, m);
     if (st != GS_OK) throw Fail{st};
     GS_CUDA(cudaStreamSynchronize(e->stream));
+    latest_stats(e);
     harvest_timing(e);
     check_stats(e);
     if (out) *out = *e->h_stats;
@@ -1462,6 +1517,7 @@ extern "C" gs_status gs_engine_update_device(gs_engine* e, const double* d_sig, 
     launch_update(e, d_sig, (const WinRec*)d_records, m);
     GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
                             cudaMemcpyDeviceToHost, e->stream));
+    e->ring_latest = false;
   });
 }
 
@@ -1490,6 +1546,7 @@ extern "C" gs_status gs_engine_resolve_host(gs_engine* e, const double* signals,
     launch_update(e, d_sig, d_rec, m);
     GS_CUDA(cudaMemcpyAsync(e->h_stats, e->S.stats, sizeof(gs_batch_stats),
                             cudaMemcpyDeviceToHost, e->stream));
+    e->ring_latest = false;
     GS_CUDA(cudaStreamSynchronize(e->stream));
     check_stats(e);
     if (out) *out = *e->h_stats;
@@ -1550,6 +1607,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     GS_CUDA(cudaStreamSynchronize(st));
     e->next_id = e->n_edges = e->n_units = 0;
     e->pf_left = e->pf_next = 0;
+    e->reset_seq = e->issued;
     memset(e->h_stats, 0, sizeof(gs_batch_stats));
     harvest_timing(e);
     e->find_ms = e->update_ms = 0.0;

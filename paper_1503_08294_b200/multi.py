@@ -177,18 +177,23 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     # the batches that really ran and halts after convergence
     lookahead = 8 if (sampler is not None and params.batch_floor == params.batch_cap) else 0
     if lookahead:
+        # room for the batches in flight up front (no growth inside the loop)
+        net.reserve(net.next_id + params.batch_cap * (lookahead + 2))
         net.set_async(lookahead)
     t_start = perf()
     if lookahead:
         m = params.batch_cap
         enq = 0
+        seq = C.c_int64()
         while enq * m < params.max_signals:
             _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
             enq += 1
-            if enq % lookahead == 0:
-                _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
-                if st.converged:
-                    break
+            # the batch issued `lookahead - 1` steps ago: waiting for it keeps
+            # the newer ones queued, so the GPU never drains
+            _lib.check(lib.gs_engine_stats_lagged(net.handle, lookahead - 1, C.byref(st),
+                                                  C.byref(seq)))
+            if seq.value >= 0 and st.converged:
+                break
         _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
         net.set_async(0)
         net._touch()
