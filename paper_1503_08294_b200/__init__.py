@@ -18,22 +18,36 @@ from .params import (
     batch_size,
 )
 from .sampling import CloudSource, DoubleTorusSource, MeshSource, SphereSource, TorusSource
-from .metrics import RunStats, TriMesh, extract_mesh, genus, manifold_check, write_stats_csv
+from .metrics import (
+    RunStats,
+    TriMesh,
+    extract_mesh,
+    genus,
+    manifold_check,
+    quantization_error,
+    write_stats_csv,
+)
+from .fileio import ParseError, load_off, load_xyz, save_off, save_xyz
 from ._lib import DeviceUnavailable, FIND_AUTO, FIND_EXACT, FIND_FILTER
 from .network import Network, Snapshot
 from .multi import (
+    ExecConfig,
     b200_executor,
+    parallel_batch_find_winners,
+    timed_find,
     batch_find_winners,
     parallel_executor,
     resolve_and_update,
     run_multi,
     sequential_executor,
 )
-from .engine import find_winners_exhaustive, is_converged, update_single
+from .engine import find_winners_exhaustive, is_converged, run, update_single
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "ExecConfig", "ParseError", "load_off", "load_xyz", "save_off", "save_xyz",
+    "parallel_batch_find_winners", "quantization_error", "run", "timed_find",
     "BatchOutcome", "CloudSource", "DeviceUnavailable", "DoubleTorusSource", "EngineParams",
     "FIND_AUTO", "FIND_EXACT", "FIND_FILTER", "MeshSource", "Network", "RingClass", "RunStats",
     "Snapshot", "SphereSource", "StateError", "TorusSource", "TriMesh", "UnknownUnitError",

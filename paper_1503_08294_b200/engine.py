@@ -16,7 +16,7 @@ from .multi import RunState, resolve_and_update
 from .network import Network, Snapshot
 from .params import EngineParams, StateError, WinnerResult
 
-__all__ = ["find_winners_exhaustive", "update_single", "is_converged", "RunState"]
+__all__ = ["find_winners_exhaustive", "update_single", "is_converged", "RunState", "run"]
 
 
 def find_winners_exhaustive(snapshot: Snapshot, signal, backend=None) -> WinnerResult:
@@ -46,3 +46,69 @@ def is_converged(net: Network, params: EngineParams) -> bool:
         return False
     ok = c["disk"] + (c["half"] if params.allow_boundary else 0)
     return ok == c["units"] and c["untrained"] == 0
+
+
+def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, backend=None,
+        checkpoints=(), variant: str | None = None, dataset: str | None = None):
+    """The single-signal engine (engine.py:368-462) on the device.
+
+    One signal per iteration, exhaustive winners against the current network,
+    update_single, convergence after every signal: exactly the multi-signal
+    loop with a batch of one (the winner lock never triggers), so it runs on
+    the same device engine and matches the reference run bit for bit.
+    ``checkpoints`` records (units, signals, sample_s, find_s, update_s,
+    total_s) the first time the unit count reaches each value.  The
+    approximate hash-grid variant (use_grid=True, grid.py) is out of scope.
+    """
+    import ctypes as C
+    import time
+    from dataclasses import replace
+
+    from . import _lib
+    from .metrics import RunStats
+
+    if use_grid:
+        raise ValueError("the approximate hash-grid (indexed) variant is not provided; "
+                         "use_grid=False runs the exact single-signal engine")
+    lib = _lib.load_library()
+    p1 = replace(params, batch_floor=1, batch_cap=1)
+    rng = np.random.Generator(np.random.Philox(seed))
+    net = Network(p1)
+    net.watch_age_limit(params.max_age)
+    seeds = source.sample(rng, 2)
+    for k in range(2):
+        net.add_unit(seeds[k], params.theta0)
+    cps = list(checkpoints)
+    records = []
+    phase = np.zeros(2, np.float64)
+    _lib.check(lib.gs_engine_phase_ms(net.handle, 1, phase))
+    st = _lib.GsBatchStats()
+    signals = 0
+    converged = False
+    sample_s = 0.0
+    perf = time.perf_counter
+    t_start = perf()
+    while signals < params.max_signals:
+        t0 = perf()
+        xi = np.ascontiguousarray(source.sample(rng, 1), dtype=np.float64)
+        sample_s += perf() - t0
+        _lib.check(lib.gs_engine_step(net.handle, xi, 1, C.byref(st)))
+        signals += 1
+        while cps and int(st.units) >= cps[0]:
+            _lib.check(lib.gs_engine_phase_ms(net.handle, -1, phase))
+            records.append((int(st.units), signals, sample_s, phase[0] * 1e-3, phase[1] * 1e-3,
+                            perf() - t_start))
+            cps.pop(0)
+        if st.converged:
+            converged = True
+            break
+    total = perf() - t_start
+    _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
+    net._touch()
+    stats = RunStats(variant=variant or "single", dataset=dataset or getattr(source, "label", "unknown"),
+                     seed=seed, iterations=signals, signals=signals, discarded=0,
+                     units=int(st.units), connections=int(st.edges), total_s=total,
+                     sample_s=sample_s, find_s=phase[0] * 1e-3, update_s=phase[1] * 1e-3,
+                     converged=converged)
+    stats.checkpoints = records
+    return net, stats

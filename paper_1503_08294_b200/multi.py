@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -36,6 +37,9 @@ __all__ = [
     "b200_executor",
     "sequential_executor",
     "parallel_executor",
+    "ExecConfig",
+    "parallel_batch_find_winners",
+    "timed_find",
     "resolve_and_update",
     "run_multi",
     "RunState",
@@ -89,9 +93,44 @@ def b200_executor(tile: int | None = None):
 sequential_executor = b200_executor
 
 
-def parallel_executor(cfg=None, backend=None):
+@dataclass(frozen=True)
+class ExecConfig:
+    """parallel.py:34-49: worker count and tile length.  Validated like the
+    reference's; the B200 scan's parallelism is the GPU's, so neither value
+    changes the work (and no value changes a result)."""
+
+    workers: int = 0
+    tile: int = 1024
+
+    def __post_init__(self):
+        if self.workers < 0:
+            raise ValueError("workers must be >= 0")
+        if self.tile < 1:
+            raise ValueError("tile must be >= 1")
+
+    def effective_workers(self, m: int) -> int:
+        import os
+
+        return max(1, min(self.workers or os.cpu_count() or 1, m))
+
+
+def parallel_batch_find_winners(snapshot: Snapshot, batch, cfg: ExecConfig | None = None,
+                                backend=None) -> list[WinnerResult]:
+    """parallel.py:91-97 on the B200 scan."""
+    cfg = cfg or ExecConfig()
+    return batch_find_winners(snapshot, batch, tile=cfg.tile)
+
+
+def timed_find(snapshot: Snapshot, batch, cfg: ExecConfig | None = None, backend=None):
+    """parallel.py:100-104: (winners, seconds) of one batched find."""
+    t0 = time.perf_counter()
+    winners = parallel_batch_find_winners(snapshot, batch, cfg, backend)
+    return winners, time.perf_counter() - t0
+
+
+def parallel_executor(cfg: ExecConfig | None = None, backend=None):
     """parallel.py:107-114 equivalent: the parallelism is the GPU's."""
-    return b200_executor()
+    return b200_executor(tile=(cfg or ExecConfig()).tile)
 
 
 def _winner_arrays(winners):
