@@ -518,6 +518,70 @@ __device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, 
   return __shfl_sync(0xffffffffu, fired, 0);
 }
 
+// adapt_threshold outcome (engine.py:208-265) of committed signal jj with
+// winner b, from the window-start state: -2 none, else patience | shrink << 30.
+// Evaluated in C1 (not B): it never makes an event, so it stays off B's
+// critical path and overlaps C1's own loads.
+__device__ int adapt_outcome(const DevState& S, const Params& P, int b, int jj, bool hb_low) {
+  const int ringb = S.ring[b], patb = S.patience[b];
+  const int db = S.deg[b];
+  const int2* B = S.adj + (size_t)b * kMaxDeg;
+  int pat = -2;
+  if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) {
+    pat = 0;
+  } else if (hb_low) {
+    // every neighbour must be trained at time jj (engine.py:225-231):
+    // neighbours' habituation loads issue together per chunk; only the
+    // untrained-at-window-start ones need their decays replayed
+    bool ok = true;
+    for (int c0 = 0; c0 < db && ok; c0 += kStage) {
+      const int dc = min(kStage, db - c0);
+      int2 nb[kStage];
+      stage_adj(B + c0, dc, nb);
+      double hv0[kStage];
+#pragma unroll
+      for (int k = 0; k < kStage; ++k) hv0[k] = k < dc ? S.hab[nb[k].x] : 0.0;
+#pragma unroll 1
+      for (int k = 0; k < dc && ok; ++k) {
+        const double hvT = hv0[k];
+        if (hvT < P.h_t) continue;
+        const int v = nb[k].x;
+        const int jv = S.firstwin[v];
+        const bool vwon = jv < jj;
+        const int dv = S.deg[v];
+        const int2* V = S.adj + (size_t)v * kMaxDeg;
+        int k1 = 0, k2 = 0;
+        for (int q0 = 0; q0 < dv; q0 += kStage) {
+          const int dq = min(kStage, dv - q0);
+          int2 wb[kStage];
+          stage_adj(V + q0, dq, wb);
+          int jw[kStage];
+#pragma unroll
+          for (int q = 0; q < kStage; ++q) jw[q] = q < dq ? S.firstwin[wb[q].x] : kNone32;
+#pragma unroll
+          for (int q = 0; q < kStage; ++q) {
+            if (q < dq && jw[q] <= jj) {
+              if (vwon && jw[q] > jv) k2++;
+              else k1++;
+            }
+          }
+        }
+        double hv = pow_chain(hvT, P.c_n, k1);
+        if (vwon) hv = dmul(hv, P.c_b);
+        hv = pow_chain(hv, P.c_n, k2);
+        if (hv >= P.h_t) ok = false;
+      }
+    }
+    if (ok) {
+      int cnt = patb + 1;
+      const int shrink = cnt >= P.ring_patience ? 1 : 0;
+      if (shrink) cnt = 0;
+      pat = cnt | (shrink << 30);
+    }
+  }
+  return pat;
+}
+
 // ---------------------------------------------------------------------------
 // cluster primitives: kCluster CTAs x 1024 threads cooperate on one window;
 // cross-CTA values travel through distributed shared memory and every
@@ -631,7 +695,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_cta[2][kCluster];
   __shared__ long long s_ctal[2][kCluster];
   __shared__ int s_plist[kUpdThreads];  // this CTA's slice of the window's processed list
-  __shared__ int s_pat[kUpdThreads];    // adapt_threshold outcome: -2 none, else patience | shrink<<30
+  __shared__ unsigned char s_hblow[kUpdThreads];  // B: winner trained at its own time
   __shared__ unsigned char s_abs[kUpdThreads];  // last_active absent at window start: b | s<<1
   __shared__ int s_walk[kWalkCap];  // units this CTA queued for replay
   __shared__ int s_nwalk;
@@ -739,7 +803,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       const double hbT = S.hab[b];
       const double thb = S.theta[b];
       const long long la_b = S.la_val[b], la_s = S.la_val[s];
-      const int ringb = S.ring[b], patb = S.patience[b];
       const bool b_trained = hbT < P.h_t;
       bool found = false;
       int kcn = 0;
@@ -779,62 +842,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (!found) ev = true;  // connect_or_reset creates b-s
       const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, kcn), P.c_b) < P.h_t;
       if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
-      int pat = -2;
-      if (!ev) {
-        if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) {
-          pat = 0;
-        } else if (hb_low) {
-          // every neighbour must be trained at time jj (engine.py:225-231):
-          // neighbours' habituation loads issue together per chunk; only the
-          // untrained-at-window-start ones need their decays replayed
-          bool ok = true;
-          for (int c0 = 0; c0 < db && ok; c0 += kStage) {
-            const int dc = min(kStage, db - c0);
-            int2 nb[kStage];
-            stage_adj(B + c0, dc, nb);
-            double hv0[kStage];
-#pragma unroll
-            for (int k = 0; k < kStage; ++k) hv0[k] = k < dc ? S.hab[nb[k].x] : 0.0;
-#pragma unroll 1
-            for (int k = 0; k < dc && ok; ++k) {
-              const double hvT = hv0[k];
-              if (hvT < P.h_t) continue;
-              const int v = nb[k].x;
-              const int jv = S.firstwin[v];
-              const bool vwon = jv < jj;
-              const int dv = S.deg[v];
-              const int2* V = S.adj + (size_t)v * kMaxDeg;
-              int k1 = 0, k2 = 0;
-              for (int q0 = 0; q0 < dv; q0 += kStage) {
-                const int dq = min(kStage, dv - q0);
-                int2 wb[kStage];
-                stage_adj(V + q0, dq, wb);
-                int jw[kStage];
-#pragma unroll
-                for (int q = 0; q < kStage; ++q) jw[q] = q < dq ? S.firstwin[wb[q].x] : kNone32;
-#pragma unroll
-                for (int q = 0; q < kStage; ++q) {
-                  if (q < dq && jw[q] <= jj) {
-                    if (vwon && jw[q] > jv) k2++;
-                    else k1++;
-                  }
-                }
-              }
-              double hv = pow_chain(hvT, P.c_n, k1);
-              if (vwon) hv = dmul(hv, P.c_b);
-              hv = pow_chain(hv, P.c_n, k2);
-              if (hv >= P.h_t) ok = false;
-            }
-          }
-          if (ok) {
-            int cnt = patb + 1;
-            const int shrink = cnt >= P.ring_patience ? 1 : 0;
-            if (shrink) cnt = 0;
-            pat = cnt | (shrink << 30);
-          }
-        }
-      }
-      s_pat[tid] = pat;
+      s_hblow[tid] = hb_low ? 1 : 0;
       // last_active presence at the window start (dict order stamps)
       s_abs[tid] = (unsigned char)((la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0));
       if (ev) evr = r;
@@ -862,7 +870,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (absent & 2) atomicMin(&S.la_stamp[cw.s], 3 * ctick + 1);
       atomicMax(&S.la_val[cw.b], ctick);
       atomicMax(&S.la_val[cw.s], ctick);
-      const int p = s_pat[tid];
+      const int p = adapt_outcome(S, P, cw.b, cj, s_hblow[tid] != 0);
       if (p != -2) {
         S.patience[cw.b] = p & 0x3fffffff;
         if (p >> 30) S.theta[cw.b] = dmul(S.theta[cw.b], P.rho);
