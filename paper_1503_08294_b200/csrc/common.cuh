@@ -94,20 +94,41 @@ struct Best2 {
 // ---------------------------------------------------------------------------
 // growable device buffer (never shrinks; contents not preserved on growth)
 
+// Stream-ordered allocations from a per-device caching pool (release
+// threshold unbounded): engines and samplers are created and closed per run,
+// and cudaMalloc/cudaFree of their arrays (a device-wide synchronisation and
+// an unmap each) cost more than a short run. dfree is ordered after the work
+// already queued on `st`; memory then returns to the pool, not the driver.
+void* dmalloc(size_t bytes, cudaStream_t st);
+void dfree(void* p, cudaStream_t st);
+// pinned host staging, cached by size for the same reason
+void* hmalloc(size_t bytes);
+void hfree(void* p);
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  cudaStream_t st = nullptr;  // set: pool allocations ordered on st; null: cudaMalloc
   void* get(size_t bytes) {
     if (bytes > cap) {
-      if (p) GS_CUDA(cudaFree(p));
-      p = nullptr;
-      cap = bytes + bytes / 2 + 256;
-      GS_CUDA(cudaMalloc(&p, cap));
+      release();
+      const size_t want = bytes + bytes / 2 + 256;
+      if (st) {
+        p = dmalloc(want, st);
+      } else {
+        GS_CUDA(cudaMalloc(&p, want));
+      }
+      cap = want;
     }
     return p;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (st)
+        dfree(p, st);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
   }

@@ -1,6 +1,8 @@
 // ctx.cu -- context lifetime, error strings, launch accounting.
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <unordered_map>
 
 #include "common.cuh"
 
@@ -11,6 +13,66 @@ unsigned long long g_launches = 0;
 static thread_local std::string t_last_error;
 
 void set_error(const std::string& msg) { t_last_error = msg; }
+
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[64] = {};
+static std::multimap<size_t, void*> g_host_free;
+static std::unordered_map<void*, size_t> g_host_size;
+
+static cudaMemPool_t device_pool() {
+  int dev = 0;
+  GS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) throw Fail{GS_CUDA_ERROR};
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    GS_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = ~0ull;
+    GS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    g_pool[dev] = pool;
+  }
+  return g_pool[dev];
+}
+
+void* dmalloc(size_t bytes, cudaStream_t st) {
+  void* p = nullptr;
+  GS_CUDA(cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, device_pool(), st));
+  return p;
+}
+
+void dfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+void* hmalloc(size_t bytes) {
+  bytes = (bytes + 4095) & ~(size_t)4095;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_host_free.lower_bound(bytes);
+    if (it != g_host_free.end() && it->first <= 2 * bytes) {
+      void* p = it->second;
+      g_host_free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  GS_CUDA(cudaMallocHost(&p, bytes));
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_host_size[p] = bytes;
+  return p;
+}
+
+void hfree(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_host_size.find(p);
+  if (it == g_host_size.end()) return;
+  g_host_free.emplace(it->second, p);
+}
 
 void* Ctx::ensure_device(size_t bytes) {
   if (bytes > d_cap) {

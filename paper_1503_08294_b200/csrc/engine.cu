@@ -884,13 +884,9 @@ namespace {
 
 template <class T>
 void grow_array(T*& p, size_t old_n, size_t new_n, cudaStream_t st) {
-  T* q = nullptr;
-  GS_CUDA(cudaMalloc(&q, sizeof(T) * new_n));
+  T* q = (T*)dmalloc(sizeof(T) * new_n, st);
   if (p && old_n) GS_CUDA(cudaMemcpyAsync(q, p, sizeof(T) * old_n, cudaMemcpyDeviceToDevice, st));
-  if (p) {
-    GS_CUDA(cudaStreamSynchronize(st));
-    GS_CUDA(cudaFree(p));
-  }
+  dfree(p, st);  // ordered after the copy
   p = q;
 }
 
@@ -926,8 +922,8 @@ void grow_units(gs_engine* e, int new_u) {
   grow_array(S.touchfirst, old, new_u, st);
   grow_array(S.iso_pos, old, new_u, st);
   grow_array(S.rows, old, new_u, st);
-  if (S.rowpos) GS_CUDA(cudaFree(S.rowpos));  // regenerated by the next update (stride U)
-  GS_CUDA(cudaMalloc(&S.rowpos, sizeof(double) * 3 * (size_t)new_u));
+  dfree(S.rowpos, st);  // regenerated by the next update (stride U)
+  S.rowpos = (double*)dmalloc(sizeof(double) * 3 * (size_t)new_u, st);
   {
     const int stale = -1;
     GS_CUDA(cudaMemcpyAsync(&S.cnt->rowpos_n, &stale, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -935,8 +931,8 @@ void grow_units(gs_engine* e, int new_u) {
   }
   grow_array(S.iso_list, old, new_u, st);
   // scratch content is transient: plain reallocation
-  if (S.scratch) GS_CUDA(cudaFree(S.scratch));
-  GS_CUDA(cudaMalloc(&S.scratch, sizeof(long long) * 2 * (size_t)new_u + 64));
+  dfree(S.scratch, st);
+  S.scratch = (long long*)dmalloc(sizeof(long long) * 2 * (size_t)new_u + 64, st);
   const int64_t add = new_u - old;
   GS_CUDA(cudaMemsetAsync(S.alive + old, 0, add, st));
   GS_CUDA(cudaMemsetAsync(S.deg + old, 0, sizeof(int32_t) * add, st));
@@ -958,8 +954,7 @@ void grow_edges(gs_engine* e, int new_ec) {
   grow_array(S.eage, old, new_ec, st);
   // the free stack keeps its first efree_top entries; new ids go on top of
   // them in descending order so the lowest new id pops first
-  int32_t* nf = nullptr;
-  GS_CUDA(cudaMalloc(&nf, sizeof(int32_t) * (size_t)new_ec));
+  int32_t* nf = (int32_t*)dmalloc(sizeof(int32_t) * (size_t)new_ec, st);
   int top = 0;
   if (S.efree) {
     Counters hc;
@@ -969,8 +964,7 @@ void grow_edges(gs_engine* e, int new_ec) {
     // existing free ids sit below; new ids above (popped first) - order of
     // edge ids is never observable
     if (top) GS_CUDA(cudaMemcpyAsync(nf, S.efree, sizeof(int32_t) * top, cudaMemcpyDeviceToDevice, st));
-    GS_CUDA(cudaStreamSynchronize(st));
-    GS_CUDA(cudaFree(S.efree));
+    dfree(S.efree, st);
   }
   S.efree = nf;
   k_push_free<<<64, 256, 0, st>>>(S.efree, top, old, new_ec);
@@ -1154,23 +1148,25 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
     }
     try {
       GS_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-      GS_CUDA(cudaMalloc(&e->S.cnt, sizeof(Counters)));
+      cudaStream_t st = e->stream;
+      for (DevBuf* b : {&e->find_work, &e->sig_buf, &e->rec_buf, &e->idx_buf}) b->st = st;
+      e->S.cnt = (Counters*)dmalloc(sizeof(Counters), st);
       GS_CUDA(cudaMemsetAsync(e->S.cnt, 0, sizeof(Counters), e->stream));
       Counters init{};
       init.next_sweep = kSweepEvery;
       GS_CUDA(cudaMemcpyAsync(e->S.cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, e->stream));
       GS_CUDA(cudaStreamSynchronize(e->stream));
-      GS_CUDA(cudaMalloc(&e->S.stats, sizeof(gs_batch_stats)));
-      GS_CUDA(cudaMemset(e->S.stats, 0, sizeof(gs_batch_stats)));
-      GS_CUDA(cudaMalloc(&e->S.aff, sizeof(int32_t) * kAffCap));
-      GS_CUDA(cudaMalloc(&e->S.defer_list, sizeof(int32_t) * kDeferCap));
-      GS_CUDA(cudaMallocHost(&e->h_stats, sizeof(gs_batch_stats)));
+      e->S.stats = (gs_batch_stats*)dmalloc(sizeof(gs_batch_stats), st);
+      GS_CUDA(cudaMemsetAsync(e->S.stats, 0, sizeof(gs_batch_stats), st));
+      e->S.aff = (int32_t*)dmalloc(sizeof(int32_t) * kAffCap, st);
+      e->S.defer_list = (int32_t*)dmalloc(sizeof(int32_t) * kDeferCap, st);
+      e->h_stats = (gs_batch_stats*)hmalloc(sizeof(gs_batch_stats));
       memset(e->h_stats, 0, sizeof(gs_batch_stats));
-      GS_CUDA(cudaMallocHost(&e->h_ring, sizeof(gs_batch_stats) * gs_engine::kEvRing));
+      e->h_ring = (gs_batch_stats*)hmalloc(sizeof(gs_batch_stats) * gs_engine::kEvRing);
       memset(e->h_ring, 0, sizeof(gs_batch_stats) * gs_engine::kEvRing);
       for (auto& ev : e->stat_ev) GS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      GS_CUDA(cudaMalloc(&e->d_res, 4 * sizeof(long long)));
-      GS_CUDA(cudaMallocHost(&e->h_res, 4 * sizeof(long long)));
+      e->d_res = (long long*)dmalloc(4 * sizeof(long long), st);
+      e->h_res = (long long*)hmalloc(4 * sizeof(long long));
       const int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(capacity_hint, 1 << 28));
       grow_units(e, (int)cap);
       grow_edges(e, (int)std::min<int64_t>(4 * cap, 1 << 29));
@@ -1192,14 +1188,13 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
                   S.rowpos};
-  for (void* q : ptrs)
-    if (q) cudaFree(q);
-  if (e->h_stats) cudaFreeHost(e->h_stats);
-  if (e->h_ring) cudaFreeHost(e->h_ring);
+  for (void* q : ptrs) dfree(q, e->stream);  // stream is idle: back to the pool at once
+  hfree(e->h_stats);
+  hfree(e->h_ring);
   for (auto ev : e->stat_ev)
     if (ev) cudaEventDestroy(ev);
-  if (e->h_res) cudaFreeHost(e->h_res);
-  if (e->h_sig) cudaFreeHost(e->h_sig);
+  hfree(e->h_res);
+  hfree(e->h_sig);
   for (auto& trio : e->ev)
     for (auto ev : trio)
       if (ev) cudaEventDestroy(ev);
@@ -1483,9 +1478,11 @@ extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t
     GS_CHECK(e && signals && m > 0, GS_VALUE_ERROR, "bad step arguments");
     const size_t bytes = sizeof(double) * 3 * (size_t)m;
     if (bytes > e->h_sig_cap) {
-      if (e->h_sig) GS_CUDA(cudaFreeHost(e->h_sig));
+      GS_CUDA(cudaStreamSynchronize(e->stream));  // a queued copy may still read it
+      hfree(e->h_sig);
+      e->h_sig = nullptr;
       e->h_sig_cap = bytes + bytes / 2;
-      GS_CUDA(cudaMallocHost(&e->h_sig, e->h_sig_cap));
+      e->h_sig = (double*)hmalloc(e->h_sig_cap);
     }
     memcpy(e->h_sig, signals, bytes);
     double* d_sig = (double*)e->sig_buf.get(bytes);

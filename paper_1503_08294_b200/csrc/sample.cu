@@ -271,21 +271,22 @@ extern "C" gs_status gs_sampler_create(gs_ctx* ctx, const double* points, int64_
     s->ctx = ctx;
     s->npts = (unsigned long long)npts;
     try {
-      GS_CUDA(cudaMalloc(&s->d_state, sizeof(PhiloxState)));
+      s->d_state = (PhiloxState*)dmalloc(sizeof(PhiloxState), ctx->stream);
       if (!points) {
         s->d_pts = nullptr;  // index-only sampler (rng.integers(0, npts, m))
       } else if (points_on_device) {
         s->d_pts = const_cast<double*>(points);
       } else {
-        GS_CUDA(cudaMalloc(&s->d_pts, sizeof(double) * 3 * (size_t)npts));
+        s->d_pts = (double*)dmalloc(sizeof(double) * 3 * (size_t)npts, ctx->stream);
         s->owns_pts = true;
         GS_CUDA(cudaMemcpyAsync(s->d_pts, points, sizeof(double) * 3 * (size_t)npts,
                                 cudaMemcpyHostToDevice, ctx->stream));
-        GS_CUDA(cudaStreamSynchronize(ctx->stream));
       }
+      GS_CUDA(cudaStreamSynchronize(ctx->stream));  // draws run on other streams
     } catch (...) {
-      if (s->d_state) cudaFree(s->d_state);
-      if (s->owns_pts && s->d_pts) cudaFree(s->d_pts);
+      cudaStreamSynchronize(ctx->stream);
+      dfree(s->d_state, ctx->stream);
+      if (s->owns_pts) dfree(s->d_pts, ctx->stream);
       delete s;
       throw;
     }
@@ -296,8 +297,10 @@ extern "C" gs_status gs_sampler_create(gs_ctx* ctx, const double* points, int64_
 extern "C" void gs_sampler_destroy(gs_sampler* s) {
   if (!s) return;
   cudaSetDevice(s->ctx->device);
-  if (s->d_state) cudaFree(s->d_state);
-  if (s->owns_pts && s->d_pts) cudaFree(s->d_pts);
+  // draws run on caller streams: wait for them before the memory returns to the pool
+  cudaDeviceSynchronize();
+  dfree(s->d_state, s->ctx->stream);
+  if (s->owns_pts) dfree(s->d_pts, s->ctx->stream);
   s->idx_tmp.release();
   delete s;
 }
