@@ -272,6 +272,272 @@ __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-n screened find (GS_FIND_SMALL; AUTO for n <= 4096): one kernel, the
+// same output bit for bit.  Every CTA stages all rows in shared memory as FP32
+// unit pairs relative to a centre c (row 0 rounded to FP32, so c is exact in
+// binary64): {-2P'x, -2P'y, -2P'z, |P'|^2}, P' = fl32(p - c).  A warp owns FS
+// signals; lane l owns the unit pairs l, l+32, ... .
+//   pass 1  e = |P'|^2 - 2 P'.Q' with three packed FFMA2 per two units and a
+//           running minimum: no indices, no branches.
+//   screen  e2 = the second smallest of the 32 lane minima.  Two distinct
+//           units have e_fp32 <= e2, so with f >= |e_fp32 - e_real| for every
+//           unit (filter.cu's bound with a = Pmax) the reference's best two
+//           both have e_fp32 <= T = e2 + 2f (+ FP64 slack).  Only lanes whose
+//           minimum is <= T can hold one; their units are re-screened one by
+//           one and those with e_fp32 <= T form the warp's candidate list
+//           (usually two or three per signal).
+//   exact   every candidate is evaluated in FP64 with the reference rounding
+//           (one per lane) and lane k merges signal k's candidates in
+//           lexicographic (d2, row) order.
+// Whenever the bound does not apply (fewer than two finite FP32 values,
+// non-finite or huge coordinates) or the list overflows (mass ties), the
+// warp scans every row exactly instead.
+
+constexpr int kSfThreads = 256;
+constexpr int kSfWarps = kSfThreads / 32;
+constexpr int kSfMaxRows = 4096;  // 16 B per row in shared memory
+constexpr int kSfCand = 128;      // candidate list per warp
+
+__device__ __forceinline__ void warp_best2_merge(Best2& b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double od1 = __shfl_xor_sync(0xffffffffu, b.d1, o);
+    const double od2 = __shfl_xor_sync(0xffffffffu, b.d2, o);
+    const int32_t oi1 = __shfl_xor_sync(0xffffffffu, b.i1, o);
+    const int32_t oi2 = __shfl_xor_sync(0xffffffffu, b.i2, o);
+    best2_lex(b, od1, oi1);
+    best2_lex(b, od2, oi2);
+  }
+}
+
+__device__ __forceinline__ bool sf_row(const FindArgs& a, bool compact, int64_t r, double& x,
+                                       double& y, double& z) {
+  if (compact) {
+    x = a.rowpos[r];
+    y = a.rowpos[a.rowpos_stride + r];
+    z = a.rowpos[2 * a.rowpos_stride + r];
+    return true;
+  }
+  return load_row(a, r, x, y, z);
+}
+
+template <int kFS>
+__global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, int tile_rows) {
+  extern __shared__ __align__(16) float4 s_u[];  // A0[npad] {ax0,ax1,ay0,ay1}, A1[npad] {az0,az1,w0,w1}
+  __shared__ float s_pm[kSfWarps];
+  __shared__ int32_t s_cand[kSfWarps][kSfCand];  // row * 4 + signal slot
+  __shared__ double s_d[kSfWarps][kSfCand];
+  __shared__ double s_q[kSfWarps][kFS][3];
+  const int npad = tile_rows / 2;  // unit pairs (tile_rows is a multiple of 128)
+  float4* A0 = s_u;
+  float4* A1 = s_u + npad;
+  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t sig0 = ((int64_t)blockIdx.x * kSfWarps + warp) * kFS;
+  const bool compact = a.rowpos && *a.rowpos_n == n;
+
+  // signals (FP64, as the reference reads them)
+  double qx[kFS], qy[kFS], qz[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + k;
+    qx[k] = qy[k] = qz[k] = 0.0;
+    if (j < a.m) {
+      if (a.sig_idx) {  // fused sampling: gather, one lane stores the signal
+        const size_t src = 3 * (size_t)a.sig_idx[j];
+        qx[k] = a.sig_pts[src];
+        qy[k] = a.sig_pts[src + 1];
+        qz[k] = a.sig_pts[src + 2];
+        if (lane == 0) {
+          double* o = const_cast<double*>(a.sig);
+          o[3 * j] = qx[k];
+          o[3 * j + 1] = qy[k];
+          o[3 * j + 2] = qz[k];
+        }
+      } else {
+        qx[k] = a.sig[3 * j];
+        qy[k] = a.sig[3 * j + 1];
+        qz[k] = a.sig[3 * j + 2];
+      }
+    }
+  }
+  bool full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
+  if (!full_scan) {
+    const int nr = (int)n;
+    // centre: row 0 rounded to FP32 (any centre is valid; the bound uses Pmax)
+    double cx = 0.0, cy = 0.0, cz = 0.0;
+    if (nr > 0) {
+      double x, y, z;
+      if (sf_row(a, compact, 0, x, y, z) && fabs(x) < 1e30 && fabs(y) < 1e30 && fabs(z) < 1e30) {
+        cx = (double)__double2float_rn(x);
+        cy = (double)__double2float_rn(y);
+        cz = (double)__double2float_rn(z);
+      }
+    }
+    // stage the FP32 unit pairs; max-norm of P' for Pmax
+    float pm = 0.f;
+    for (int p = threadIdx.x; p < npad; p += kSfThreads) {
+      float ax[2], ay[2], az[2], w[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 2 * p + h;
+        ax[h] = ay[h] = az[h] = 0.f;
+        w[h] = INFINITY;
+        double x, y, z;
+        // a row with a non-finite coordinate has d2 = inf or NaN for every
+        // signal and is never selected (nor are the update's dead rows,
+        // stored as +inf): it is left out like a dead one
+        if (r < nr && sf_row(a, compact, r, x, y, z) && isfinite(x) && isfinite(y) &&
+            isfinite(z)) {
+          const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
+                      pz = __double2float_rn(z - cz);
+          ax[h] = -2.f * px;
+          ay[h] = -2.f * py;
+          az[h] = -2.f * pz;
+          w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
+          const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+          pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
+        }
+      }
+      A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
+      A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    if (lane == 0) s_pm[warp] = pm;
+    __syncthreads();
+    pm = s_pm[0];
+#pragma unroll
+    for (int k = 1; k < kSfWarps; ++k) pm = fmaxf(pm, s_pm[k]);
+    // |p - c| <= sqrt(3) * max_k |P'_k| / (1 - u), rounded up generously
+    const double pmax = (double)pm * 1.7320508075688774 * (1.0 + 1e-6);
+
+    // pass 1: lane minima of e
+    float2 fq[kFS][3];
+    float m1[kFS];
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) {
+      const float fx = __double2float_rn(qx[k] - cx), fy = __double2float_rn(qy[k] - cy),
+                  fz = __double2float_rn(qz[k] - cz);
+      fq[k][0] = make_float2(fx, fx);
+      fq[k][1] = make_float2(fy, fy);
+      fq[k][2] = make_float2(fz, fz);
+      m1[k] = INFINITY;
+    }
+    const int np64 = (((nr + 1) / 2) + 63) & ~63;  // padded pairs are +inf
+#pragma unroll 1
+    for (int p = lane; p < np64; p += 64) {
+      const float4 a0 = A0[p], a1 = A1[p];
+      const float4 c0 = A0[p + 32], c1 = A1[p + 32];
+#pragma unroll
+      for (int k = 0; k < kFS; ++k) {
+        float2 ea = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
+        float2 ec = __ffma2_rn(make_float2(c0.x, c0.y), fq[k][0], make_float2(c1.z, c1.w));
+        ea = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], ea);
+        ec = __ffma2_rn(make_float2(c0.z, c0.w), fq[k][1], ec);
+        ea = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], ea);
+        ec = __ffma2_rn(make_float2(c1.x, c1.y), fq[k][2], ec);
+        m1[k] = fminf(m1[k], fminf(fminf(ea.x, ea.y), fminf(ec.x, ec.y)));
+      }
+    }
+    // screen: thresholds, then the surviving lanes' units one by one
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) {
+      float v1 = m1[k], v2 = INFINITY;  // two smallest lane minima
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float o1 = __shfl_xor_sync(0xffffffffu, v1, o);
+        const float o2 = __shfl_xor_sync(0xffffffffu, v2, o);
+        v2 = fminf(fmaxf(v1, o1), fminf(v2, o2));
+        v1 = fminf(v1, o1);
+      }
+      const double Qx = qx[k] - cx, Qy = qy[k] - cy, Qz = qz[k] - cz;
+      const double q2 = Qx * Qx + Qy * Qy + Qz * Qz;
+      if (!(v2 < INFINITY && pmax * pmax <= 1e30 && q2 <= 1e30)) {
+        full_scan = true;  // warp-uniform
+        continue;
+      }
+      const double u = 0x1p-24, Q = sqrt(q2), av = pmax;
+      const double dl = u * (1.0 + u) * pmax + u * av;
+      const double f =
+          (2.0 * dl * (av + Q) + dl * dl + 6.02 * u * av * av + 8.03 * u * av * Q) * (1.0 + 1e-6) +
+          1e-44;
+      const double e2 = (double)v2;
+      const float T = __double2float_ru(e2 + 2.0 * f + 1e-14 * (fabs(e2) + f + q2));
+      unsigned tasks = __ballot_sync(0xffffffffu, m1[k] <= T);
+      while (tasks) {
+        const int l = __ffs(tasks) - 1;
+        tasks &= tasks - 1;
+        for (int i0 = 0; i0 < np64 / 32; i0 += 32) {  // lane l's pairs l + 32 i, one per lane
+          const int p = 32 * (i0 + lane) + l;
+          const bool in = p < np64;
+          const float4 a0 = in ? A0[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 a1 = in ? A1[p] : make_float4(0.f, 0.f, INFINITY, INFINITY);
+          float2 e = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
+          e = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], e);
+          e = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], e);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool pass = in && (h ? e.y : e.x) <= T;
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+            if (pass && at < kSfCand) s_cand[warp][at] = (2 * p + h) * 4 + k;
+            cnt += __popc(bal);
+          }
+        }
+      }
+      if (lane == 0) {
+        s_q[warp][k][0] = qx[k];
+        s_q[warp][k][1] = qy[k];
+        s_q[warp][k][2] = qz[k];
+      }
+    }
+    if (!full_scan && cnt <= kSfCand) {
+      __syncwarp();
+      for (int c = lane; c < cnt; c += 32) {  // exact FP64 distance per candidate
+        const int code = s_cand[warp][c];
+        const int r = code >> 2, k = code & 3;
+        double x, y, z;
+        double d = __longlong_as_double(0x7ff8000000000000LL);  // NaN: never selected
+        if (sf_row(a, compact, r, x, y, z))
+          d = dist2_exact(x, y, z, s_q[warp][k][0], s_q[warp][k][1], s_q[warp][k][2]);
+        s_d[warp][c] = d;
+      }
+      __syncwarp();
+      if (lane < kFS) {
+        Best2 b;
+        b.init();
+        for (int c = 0; c < cnt; ++c) {
+          const int code = s_cand[warp][c];
+          if ((code & 3) == lane) best2_lex(b, s_d[warp][c], code >> 2);
+        }
+        const int64_t j = sig0 + lane;
+        if (j < a.m) write_result(a, j, b);
+      }
+      return;
+    }
+    full_scan = true;
+  }
+  // exact FP64 scan of every row (stale estimate, degenerate inputs, mass ties)
+  Best2 b[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) b[k].init();
+  for (int64_t r = lane; r < n; r += 32) {
+    double x, y, z;
+    if (!sf_row(a, compact, r, x, y, z)) continue;
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) b[k].push(dist2_exact(x, y, z, qx[k], qy[k], qz[k]), (int32_t)r);
+  }
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    warp_best2_merge(b[k]);
+    const int64_t j = sig0 + k;
+    if (lane == 0 && j < a.m) write_result(a, j, b[k]);
+  }
+}
+
 // materialise sampled signals (sig[j] = pts[idx[j]]) for the non-fused finds
 __global__ void k_gather_signals(const int64_t* idx, const double* pts, double* sig, int64_t m) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -302,6 +568,46 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
   if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
       find_filter_launch(ctx, a, stream, work))
     return;
+  if (a.mode != GS_FIND_EXACT && a.n <= kSfMaxRows) {
+    static bool sf_attr = false;
+    if (!sf_attr) {
+      const int bytes = 16 * kSfMaxRows;
+      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<4>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      sf_attr = true;
+    }
+    // rows staged: the estimate plus headroom for growth in flight, a
+    // multiple of 128 (whole 64-pair steps)
+    const int tile_rows = (int)std::min<int64_t>(
+        kSfMaxRows, ((std::max<int64_t>(a.n, 1) + 512 + 127) / 128) * 128);
+    const size_t smem = 16 * (size_t)tile_rows;
+    const int64_t warps = kSfThreads / 32;
+    // signals per warp: the most that still gives every SM a CTA
+    static int fs_env = -1;
+    if (fs_env < 0) {
+      const char* e = getenv("GS_SF_FS");
+      fs_env = e ? atoi(e) : 0;
+    }
+    int fs = fs_env;
+    if (fs != 1 && fs != 2 && fs != 4) {
+      const int64_t sms = ctx.sm_count;
+      fs = (a.m * 100 >= 85 * warps * 4 * sms) ? 4 : (a.m * 100 >= 85 * warps * 2 * sms) ? 2 : 1;
+    }
+    const unsigned grid = (unsigned)((a.m + warps * fs - 1) / (warps * fs));
+    if (fs == 4)
+      find_small_f32_kernel<4><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+    else if (fs == 2)
+      find_small_f32_kernel<2><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+    else
+      find_small_f32_kernel<1><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+    GS_CUDA(cudaGetLastError());
+    ++g_launches;
+    return;
+  }
   if (a.n <= kSmallMaxRows) {
     static bool attr_set = false;
     if (!attr_set) {
@@ -432,7 +738,7 @@ extern "C" gs_status gs_find_device(gs_ctx* ctx, const double* d_pos, int64_t n,
   return guarded([&] {
     GS_CHECK(ctx, GS_VALUE_ERROR, "null context");
     GS_CHECK(n >= 0 && m >= 0, GS_VALUE_ERROR, "negative size");
-    GS_CHECK(mode >= 0 && mode <= 2, GS_VALUE_ERROR, "bad find mode");
+    GS_CHECK(mode >= 0 && mode <= 3, GS_VALUE_ERROR, "bad find mode");
     FindArgs a;
     a.pos = d_pos;
     a.n = n;
