@@ -1084,7 +1084,9 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   // host estimate of the row count (grid sizing, staging); with batches in
   // flight it can lag the device's count, which every find kernel reads
   // (n_dev) and handles past the estimate
-  a.n = e->next_id;
+  // rows hold the live units plus dead entries up to 1/8 of the rows (lazy
+  // compaction in the update), and never more than next_id
+  a.n = std::min<int64_t>(e->next_id, (int64_t)e->n_units + (e->n_units + 6) / 7 + 1);
   a.n_dev = &e->S.cnt->nrows;  // exact row count, read on the device
   a.rowpos = e->S.rowpos;
   a.rowpos_n = &e->S.cnt->rowpos_n;

@@ -322,6 +322,25 @@ __device__ __forceinline__ bool sf_row(const FindArgs& a, bool compact, int64_t 
   return load_row(a, r, x, y, z);
 }
 
+// fused sampling: the gathered signals are stored for the update (last, so
+// the stores never wait on the gather ahead of the row staging)
+template <int kFS>
+__device__ __forceinline__ void sf_store_signals(const FindArgs& a, int64_t sig0, int lane,
+                                                 const double* qx, const double* qy,
+                                                 const double* qz) {
+  if (!a.sig_idx) return;
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + k;
+    if (lane == k && j < a.m) {
+      double* o = const_cast<double*>(a.sig);
+      o[3 * j] = qx[k];
+      o[3 * j + 1] = qy[k];
+      o[3 * j + 2] = qz[k];
+    }
+  }
+}
+
 template <int kFS>
 __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, int tile_rows) {
   extern __shared__ __align__(16) float4 s_u[];  // A0[npad] {ax0,ax1,ay0,ay1}, A1[npad] {az0,az1,w0,w1}
@@ -344,17 +363,11 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
     const int64_t j = sig0 + k;
     qx[k] = qy[k] = qz[k] = 0.0;
     if (j < a.m) {
-      if (a.sig_idx) {  // fused sampling: gather, one lane stores the signal
+      if (a.sig_idx) {  // fused sampling: gather (stored for the update at the end)
         const size_t src = 3 * (size_t)a.sig_idx[j];
         qx[k] = a.sig_pts[src];
         qy[k] = a.sig_pts[src + 1];
         qz[k] = a.sig_pts[src + 2];
-        if (lane == 0) {
-          double* o = const_cast<double*>(a.sig);
-          o[3 * j] = qx[k];
-          o[3 * j + 1] = qy[k];
-          o[3 * j + 2] = qz[k];
-        }
       } else {
         qx[k] = a.sig[3 * j];
         qy[k] = a.sig[3 * j + 1];
@@ -375,33 +388,54 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         cz = (double)__double2float_rn(z);
       }
     }
-    // stage the FP32 unit pairs; max-norm of P' for Pmax
+    // stage the FP32 unit pairs; max-norm of P' for Pmax.  Four pairs per
+    // thread per step with every load issued before any use (one memory
+    // latency per step, not one per row).
     float pm = 0.f;
-    for (int p = threadIdx.x; p < npad; p += kSfThreads) {
-      float ax[2], ay[2], az[2], w[2];
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int p0 = threadIdx.x; p0 < npad; p0 += 4 * kSfThreads) {
+      double X[8], Y[8], Z[8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = 2 * p + h;
-        ax[h] = ay[h] = az[h] = 0.f;
-        w[h] = INFINITY;
-        double x, y, z;
-        // a row with a non-finite coordinate has d2 = inf or NaN for every
-        // signal and is never selected (nor are the update's dead rows,
-        // stored as +inf): it is left out like a dead one
-        if (r < nr && sf_row(a, compact, r, x, y, z) && isfinite(x) && isfinite(y) &&
-            isfinite(z)) {
-          const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
-                      pz = __double2float_rn(z - cz);
-          ax[h] = -2.f * px;
-          ay[h] = -2.f * py;
-          az[h] = -2.f * pz;
-          w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
-          const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
-          pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
+      for (int t = 0; t < 8; ++t) {
+        const int r = 2 * (p0 + (t >> 1) * kSfThreads) + (t & 1);
+        X[t] = Y[t] = Z[t] = kInf;
+        if (r < nr) {
+          if (compact) {
+            X[t] = a.rowpos[r];
+            Y[t] = a.rowpos[a.rowpos_stride + r];
+            Z[t] = a.rowpos[2 * a.rowpos_stride + r];
+          } else if (!load_row(a, r, X[t], Y[t], Z[t])) {
+            X[t] = kInf;
+          }
         }
       }
-      A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
-      A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = p0 + q * kSfThreads;
+        if (p >= npad) break;
+        float ax[2], ay[2], az[2], w[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double x = X[2 * q + h], y = Y[2 * q + h], z = Z[2 * q + h];
+          ax[h] = ay[h] = az[h] = 0.f;
+          w[h] = INFINITY;
+          // a row with a non-finite coordinate has d2 = inf or NaN for every
+          // signal and is never selected (nor are dead rows, +inf here and
+          // in the update's row snapshot): it is left out like a dead one
+          if (isfinite(x) && isfinite(y) && isfinite(z)) {
+            const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
+                        pz = __double2float_rn(z - cz);
+            ax[h] = -2.f * px;
+            ay[h] = -2.f * py;
+            az[h] = -2.f * pz;
+            w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
+            const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+            pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
+          }
+        }
+        A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
+        A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
@@ -516,6 +550,7 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         const int64_t j = sig0 + lane;
         if (j < a.m) write_result(a, j, b);
       }
+      sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
       return;
     }
     full_scan = true;
@@ -536,6 +571,7 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
     const int64_t j = sig0 + k;
     if (lane == 0 && j < a.m) write_result(a, j, b[k]);
   }
+  sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
 }
 
 // materialise sampled signals (sig[j] = pts[idx[j]]) for the non-fused finds
@@ -586,7 +622,8 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
         kSfMaxRows, ((std::max<int64_t>(a.n, 1) + 512 + 127) / 128) * 128);
     const size_t smem = 16 * (size_t)tile_rows;
     const int64_t warps = kSfThreads / 32;
-    // signals per warp: the most that still gives every SM a CTA
+    // signals per warp: the most that still gives most SMs two CTAs (the
+    // second hides the first one's staging latency; measured on cfg3)
     static int fs_env = -1;
     if (fs_env < 0) {
       const char* e = getenv("GS_SF_FS");
@@ -595,7 +632,7 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
     int fs = fs_env;
     if (fs != 1 && fs != 2 && fs != 4) {
       const int64_t sms = ctx.sm_count;
-      fs = (a.m * 100 >= 85 * warps * 4 * sms) ? 4 : (a.m * 100 >= 85 * warps * 2 * sms) ? 2 : 1;
+      fs = (a.m * 100 >= 170 * warps * 4 * sms) ? 4 : (a.m * 100 >= 170 * warps * 2 * sms) ? 2 : 1;
     }
     const unsigned grid = (unsigned)((a.m + warps * fs - 1) / (warps * fs));
     if (fs == 4)
