@@ -176,35 +176,34 @@ __device__ long long block_min_ll(long long v, long long* s_ll32) {
 // All 32 lanes must call it with the same u.
 __device__ int classify_ring_warp(const DevState& S, int u, int* sh) {
   const int lane = threadIdx.x & 31;
+  // two dependent levels (u's row, then every neighbour's row), each issued
+  // speculatively together with the degree it is masked by
+  const int2* A = S.adj + (size_t)u * kMaxDeg;
   const int k = S.deg[u];
+  const int v = A[lane].x;  // slots past deg(u) are ignored below
   if (k < 2) return kRingInc;
   if (k > 32) return classify_ring(S, u);
-  const int2* A = S.adj + (size_t)u * kMaxDeg;
-  if (lane < k) sh[lane] = A[lane].x;
+  if (lane < k) sh[lane] = v;
   __syncwarp();
-  int d = 0;
-  unsigned mask = 0;
+  unsigned mask = 0;  // bit i: N(u)[i] is adjacent to this lane's neighbour
   if (lane < k) {
-    const int v = sh[lane];
-    const int dv = S.deg[v];
     const int2* V = S.adj + (size_t)v * kMaxDeg;
-    // v's row in staged chunks (loads issue together), membership against N(u)
-    for (int c0 = 0; c0 < dv && d <= 2; c0 += kStage) {
-      int2 nb[kStage];
-      stage_adj(V + c0, min(kStage, dv - c0), nb);
+    const int dv = S.deg[v];
+    int2 nb[kStage];
+    stage_adj(V, kStage, nb);
+    for (int c0 = 0;;) {
+      for (int i = 0; i < k; ++i) {
+        const int x = sh[i];
 #pragma unroll
-      for (int c = 0; c < kStage; ++c) {
-        if (c0 + c >= dv || d > 2) continue;
-        const int w = nb[c].x;
-        for (int i = 0; i < k; ++i)
-          if (sh[i] == w) {
-            ++d;
-            mask |= 1u << i;
-            break;
-          }
+        for (int c = 0; c < kStage; ++c)
+          if (c0 + c < dv && nb[c].x == x) mask |= 1u << i;
       }
+      c0 += kStage;
+      if (c0 >= dv) break;
+      stage_adj(V + c0, min(kStage, dv - c0), nb);
     }
   }
+  const int d = __popc(mask);
   const bool bad = lane < k && (d == 0 || d > 2);
   const unsigned bal_bad = __ballot_sync(0xffffffffu, bad);
   const int deg1 = __popc(__ballot_sync(0xffffffffu, lane < k && d == 1));
