@@ -273,13 +273,23 @@ __device__ int event_part1b(const DevState& S, const Params& P, int b, int s, do
 // remove_edge, age_incident, prune_winner; network.py:261-369).
 
 // slot of b in a's adjacency, or -1 (uniform)
+// deg(a) and slot `lane` of a's row issued together (one load level instead
+// of two; slots past the degree are ignored by the callers)
+__device__ __forceinline__ int2 row_lane(const DevState& S, int a, int& d) {
+  d = S.deg[a];
+  return S.adj[(size_t)a * kMaxDeg + (threadIdx.x & 31)];
+}
+
 __device__ int w_find_slot(const DevState& S, int a, int b) {
   const int lane = threadIdx.x & 31;
-  const int d = S.deg[a];
+  int d;
+  const int2 e0 = row_lane(S, a, d);
+  unsigned bal = __ballot_sync(0xffffffffu, lane < d && e0.x == b);
+  if (bal) return __ffs(bal) - 1;
   const int2* A = S.adj + (size_t)a * kMaxDeg;
-  for (int k0 = 0; k0 < d; k0 += 32) {
+  for (int k0 = 32; k0 < d; k0 += 32) {
     const int k = k0 + lane;
-    const unsigned bal = __ballot_sync(0xffffffffu, k < d && A[k].x == b);
+    bal = __ballot_sync(0xffffffffu, k < d && A[k].x == b);
     if (bal) return k0 + __ffs(bal) - 1;
   }
   return -1;
@@ -299,14 +309,16 @@ __device__ __forceinline__ void w_defer(const DevState& S, int u) {
 // common neighbours of a and b, then a and b.  stage: per-warp smem (64 ints)
 __device__ void w_defer_ring_neighborhood(const DevState& S, int a, int b, int* stage) {
   const int lane = threadIdx.x & 31;
-  const int db = S.deg[b];
+  int db, da;
+  const int2 eb = row_lane(S, b, db);
+  const int2 ea = row_lane(S, a, da);
   const int2* Bb = S.adj + (size_t)b * kMaxDeg;
-  for (int k = lane; k < db; k += 32) stage[k] = Bb[k].x;
+  if (lane < db) stage[lane] = eb.x;
+  for (int k = lane + 32; k < db; k += 32) stage[k] = Bb[k].x;
   __syncwarp();
-  const int da = S.deg[a];
   const int2* Aa = S.adj + (size_t)a * kMaxDeg;
   for (int k = lane; k < da; k += 32) {
-    const int v = Aa[k].x;
+    const int v = k < 32 ? ea.x : Aa[k].x;
     bool common = false;
     if (v != b)
       for (int q = 0; q < db; ++q) common |= stage[q] == v;
@@ -386,7 +398,8 @@ __device__ void w_remove_edge_raw(const DevState& S, int a, int b) {
 __device__ void w_age_incident(const DevState& S, const Params& P, int b, int exclude, int inc,
                                int* over, int* nover) {
   const int lane = threadIdx.x & 31;
-  const int d = S.deg[b];
+  int d;
+  const int2 e0 = row_lane(S, b, d);
   const int2* B = S.adj + (size_t)b * kMaxDeg;
   int n = 0;
   for (int k0 = 0; k0 < d; k0 += 32) {
@@ -394,7 +407,7 @@ __device__ void w_age_incident(const DevState& S, const Params& P, int b, int ex
     bool cross = false;
     int v = -1;
     if (k < d) {
-      const int2 ent = B[k];
+      const int2 ent = k0 == 0 ? e0 : B[k];
       v = ent.x;
       if (v != exclude) {
         const int old = S.eage[ent.y];
@@ -442,10 +455,11 @@ __device__ void w_event_part2(const DevState& S, const Params& P, int b, bool sw
     return;
   }
   if (S.hab[b] >= P.h_t) return;
-  const int d = S.deg[b];
+  int d;
+  const int2 e0 = row_lane(S, b, d);
   const int2* B = S.adj + (size_t)b * kMaxDeg;
   bool untrained = false;
-  for (int k = lane; k < d; k += 32) untrained |= S.hab[B[k].x] >= P.h_t;
+  for (int k = lane; k < d; k += 32) untrained |= S.hab[(k < 32 ? e0 : B[k]).x] >= P.h_t;
   if (__any_sync(0xffffffffu, untrained)) return;
   if (lane == 0) {
     int count = S.patience[b] + 1;
@@ -988,10 +1002,11 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             S.hab[r.b] = h;
             if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
           }
-          const int db = S.deg[r.b];
+          int db;
+          const int2 e0 = row_lane(S, r.b, db);
           const int2* B = S.adj + (size_t)r.b * kMaxDeg;
           for (int k = lane; k < db; k += 32) {
-            const int v = B[k].x;
+            const int v = k < 32 ? e0.x : B[k].x;
             double4 p = S.pos[v];
             move_toward(p, P.eps_n, x, y, z);
             S.pos[v] = p;
