@@ -284,7 +284,9 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
     import numpy as np
     import torch
 
-    out = {"m": m, "mode": "filter (FP32 FFMA2 + certified FP64)", "lines": []}
+    out = {"m": m, "mode": "filter (FP32 FFMA2 + certified FP64)", "lines": [],
+           "grid_mode": "exact uniform grid rebuilt per call (GS_FIND_GRID; HBM/L2-latency bound)",
+           "grid_lines": []}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     st = torch.cuda.Stream()  # a real stream: handle 0 would mean the context's own stream
     peak = 2 * 128 * ctx.sm_count * sm_mhz * 1e6 / 1e12
@@ -296,25 +298,37 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
         d2 = torch.empty((m, 2), dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
 
-        def run():
-            _lib_check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(), m,
-                                          idx.data_ptr(), d2.data_ptr(), 1, st.cuda_stream))
+        def timed(mode):
+            def run():
+                _lib_check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(), m,
+                                              idx.data_ptr(), d2.data_ptr(), mode, st.cuda_stream))
 
-        run()
-        times = []
-        for _ in range(reps):
-            with torch.cuda.stream(st):
-                flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(st)
             run()
-            e1.record(st)
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        fb2 = np.zeros(2, np.int64)
-        _lib_check(lib.gs_find_last_fallback_counts(ctx.handle, fb2))
-        ms = statistics.median(times)
+            times = []
+            for _ in range(reps):
+                with torch.cuda.stream(st):
+                    flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                run()
+                e1.record(st)
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            fb = np.zeros(2, np.int64)
+            _lib_check(lib.gs_find_last_fallback_counts(ctx.handle, fb))
+            return statistics.median(times), fb
+
+        # exact uniform grid (GS_FIND_GRID): same output, O(m) candidates
+        gms, gfb = timed(4)
+        gbytes = 24 * n + 32 * n + 56 * m  # rows read, rows in cell order, signals + results
+        out["grid_lines"].append({"n": n, "ms": gms, "signals_per_s": m / (gms * 1e-3),
+                                  "equivalent_pairs_per_s": float(n) * m / (gms * 1e-3),
+                                  "algorithmic_bytes": gbytes,
+                                  "achieved_gbs": gbytes / (gms * 1e-3) / 1e9,
+                                  "exhaustive_fallback_signals": int(gfb[0])})
+        ms, fb2 = timed(1)
+        out["grid_lines"][-1]["speedup_vs_filter"] = ms / gms
         pairs = float(n) * m
         achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
         out["lines"].append({"n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),

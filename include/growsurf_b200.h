@@ -83,7 +83,8 @@ typedef enum {
   GS_FIND_EXACT = 0,  /* FP64 scan, the reference arithmetic */
   GS_FIND_FILTER = 1, /* FP32 top-3 filter + certified FP64 re-check (bit-identical output) */
   GS_FIND_AUTO = 2,
-  GS_FIND_SMALL = 3   /* n <= 4096: one kernel, FP32 screen + exact FP64 re-evaluation (bit-identical) */
+  GS_FIND_SMALL = 3,  /* n <= 4096: one kernel, FP32 screen + exact FP64 re-evaluation (bit-identical) */
+  GS_FIND_GRID = 4    /* exact uniform grid rebuilt per call: shells until certified (bit-identical) */
 } gs_find_mode;
 
 /* d_pos: n x 3 float64 (device), d_sig: m x 3 float64 (device);

@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(HERE, "libgrowsurf_b200.so")
 
 GS_OK, GS_VALUE_ERROR, GS_STATE_ERROR, GS_CUDA_ERROR, GS_UNKNOWN_UNIT = range(5)
-FIND_EXACT, FIND_FILTER, FIND_AUTO, FIND_SMALL = 0, 1, 2, 3
+FIND_EXACT, FIND_FILTER, FIND_AUTO, FIND_SMALL, FIND_GRID = 0, 1, 2, 3, 4
 
 
 class DeviceUnavailable(RuntimeError):

@@ -198,6 +198,54 @@ struct FindArgs {
   int mode = GS_FIND_AUTO;
 };
 
+// row r of a find's unit set (false: a dead engine slot)
+__device__ __forceinline__ bool load_row(const FindArgs& a, int64_t r, double& x, double& y,
+                                         double& z) {
+  if (a.pos4) {
+    const int32_t slot = a.rows ? a.rows[r] : (int32_t)r;
+    if (a.alive && !a.alive[slot]) return false;
+    const double4 p = a.pos4[slot];
+    x = p.x;
+    y = p.y;
+    z = p.z;
+    return true;
+  }
+  x = a.pos[3 * r];
+  y = a.pos[3 * r + 1];
+  z = a.pos[3 * r + 2];
+  return true;
+}
+
+__device__ __forceinline__ void write_result(const FindArgs& a, int64_t j, const Best2& b) {
+  if (a.out_idx) {
+    a.out_idx[2 * j] = b.i1;
+    a.out_idx[2 * j + 1] = b.i2;
+    a.out_d2[2 * j] = b.d1;
+    a.out_d2[2 * j + 1] = b.d2;
+  }
+  if (a.out_win) {
+    WinRec w;
+    w.b = (b.i1 >= 0 && a.rows) ? a.rows[b.i1] : b.i1;
+    w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
+    w.dwin = __dsqrt_rn(b.d1);  // math.sqrt (correctly rounded): multi.py:72-78
+    a.out_win[j] = w;
+  }
+}
+
+// lexicographic (d2, row) insertion, any visiting order
+__device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
+  if (i < 0) return;
+  if (d < b.d1 || (d == b.d1 && i < b.i1)) {
+    b.d2 = b.d1;
+    b.i2 = b.i1;
+    b.d1 = d;
+    b.i1 = i;
+  } else if (i != b.i1 && (d < b.d2 || (d == b.d2 && i < b.i2))) {
+    b.d2 = d;
+    b.i2 = i;
+  }
+}
+
 void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 
 // device CloudSource sampler (sample.cu): m signals into d_out on `stream`

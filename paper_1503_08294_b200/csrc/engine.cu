@@ -1113,7 +1113,7 @@ void set_params(gs_engine* e, const gs_params* p) {
            GS_VALUE_ERROR, "tau_b, tau_n, h_t, rho must lie in (0, 1)");
   GS_CHECK(p->max_age >= 0 && p->ring_patience >= 1 && p->stale_factor >= 1, GS_VALUE_ERROR,
            "bad max_age / ring_patience / stale_factor");
-  GS_CHECK(p->find_mode >= 0 && p->find_mode <= 3, GS_VALUE_ERROR, "bad find mode");
+  GS_CHECK(p->find_mode >= 0 && p->find_mode <= 4, GS_VALUE_ERROR, "bad find mode");
   e->hp = *p;
   e->P.eps_b = p->eps_b;
   e->P.eps_n = p->eps_n;

@@ -33,39 +33,6 @@ struct Part {
   int32_t i1, i2;
 };
 
-__device__ __forceinline__ bool load_row(const FindArgs& a, int64_t r, double& x, double& y,
-                                         double& z) {
-  if (a.pos4) {
-    const int32_t slot = a.rows ? a.rows[r] : (int32_t)r;
-    if (a.alive && !a.alive[slot]) return false;
-    const double4 p = a.pos4[slot];
-    x = p.x;
-    y = p.y;
-    z = p.z;
-    return true;
-  }
-  x = a.pos[3 * r];
-  y = a.pos[3 * r + 1];
-  z = a.pos[3 * r + 2];
-  return true;
-}
-
-__device__ __forceinline__ void write_result(const FindArgs& a, int64_t j, const Best2& b) {
-  if (a.out_idx) {
-    a.out_idx[2 * j] = b.i1;
-    a.out_idx[2 * j + 1] = b.i2;
-    a.out_d2[2 * j] = b.d1;
-    a.out_d2[2 * j + 1] = b.d2;
-  }
-  if (a.out_win) {
-    WinRec w;
-    w.b = (b.i1 >= 0 && a.rows) ? a.rows[b.i1] : b.i1;
-    w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
-    w.dwin = __dsqrt_rn(b.d1);  // math.sqrt (correctly rounded): multi.py:72-78
-    a.out_win[j] = w;
-  }
-}
-
 template <int kFS>  // signals per thread
 __global__ void __launch_bounds__(kFT) find_exact_kernel(FindArgs a, int64_t rows_per_chunk,
                                                          Part* part) {
@@ -153,18 +120,6 @@ constexpr int kSmallThreads = 256;
 constexpr int kSmallSlices = 16;
 constexpr int kSmallMaxRows = 6144;  // 144 KB of shared memory
 
-__device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
-  if (i < 0) return;
-  if (d < b.d1 || (d == b.d1 && i < b.i1)) {
-    b.d2 = b.d1;
-    b.i2 = b.i1;
-    b.d1 = d;
-    b.i1 = i;
-  } else if (i != b.i1 && (d < b.d2 || (d == b.d2 && i < b.i2))) {
-    b.d2 = d;
-    b.i2 = i;
-  }
-}
 
 template <int kFS>
 __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, int tile_rows) {
@@ -584,13 +539,19 @@ __global__ void k_gather_signals(const int64_t* idx, const double* pts, double* 
   sig[3 * j + 2] = pts[src + 2];
 }
 
-// forward declaration (filter.cu)
+// forward declarations (filter.cu, grid.cu)
 bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
+void find_grid_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 
 void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& work) {
   if (a_in.m <= 0) return;
   FindArgs a = a_in;
-  const bool small = a.n <= kSmallMaxRows &&
+  // AUTO: the grid for large scans (its ~10 launches are amortised), which
+  // is where the FP32 filter ran before it (1e6 signals: 0.7-0.8 ms at any
+  // n from 1e4 to 1e6 against 1.8-147 ms)
+  const bool use_grid = a.mode == GS_FIND_GRID ||
+                    (a.mode == GS_FIND_AUTO && a.n > kSfMaxRows && (double)a.n * (double)a.m >= 6.0e7);
+  const bool small = !use_grid && a.n <= kSmallMaxRows &&
                      !((a.mode == GS_FIND_FILTER) || (a.mode == GS_FIND_AUTO && a.n >= 4096 &&
                                                       (double)a.n * (double)a.m >= 6.0e7));
   if (a.sig_idx && !small) {  // only the small kernel gathers in place
@@ -600,6 +561,10 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
     ++g_launches;
     a.sig_idx = nullptr;
     a.sig_pts = nullptr;
+  }
+  if (use_grid) {
+    find_grid_launch(ctx, a, stream, work);
+    return;
   }
   if ((a.mode == GS_FIND_FILTER || a.mode == GS_FIND_AUTO) &&
       find_filter_launch(ctx, a, stream, work))
@@ -775,7 +740,7 @@ extern "C" gs_status gs_find_device(gs_ctx* ctx, const double* d_pos, int64_t n,
   return guarded([&] {
     GS_CHECK(ctx, GS_VALUE_ERROR, "null context");
     GS_CHECK(n >= 0 && m >= 0, GS_VALUE_ERROR, "negative size");
-    GS_CHECK(mode >= 0 && mode <= 3, GS_VALUE_ERROR, "bad find mode");
+    GS_CHECK(mode >= 0 && mode <= 4, GS_VALUE_ERROR, "bad find mode");
     FindArgs a;
     a.pos = d_pos;
     a.n = n;

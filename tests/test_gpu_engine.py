@@ -40,7 +40,7 @@ def test_device_run_matches_reference_golden(name):
     net.audit()
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 3, 4])  # exact, filter, screened small, grid
 def test_find_modes_identical_runs(mode):
     gold = load_golden("stress")
     net, stats, per_batch, _ = run_device_trace("stress", find_mode=mode)
