@@ -50,6 +50,7 @@ struct GridMeta {
   unsigned nlive;
   unsigned nfb;   // signals scanned exhaustively
   unsigned nfb2;  // copy (gs_find_last_fallback_counts reads two words)
+  unsigned nsig;  // finite signals (queried in cell order)
   int bad;        // no usable grid: every signal is scanned exhaustively
 };
 
@@ -80,6 +81,7 @@ __global__ void k_grid_init(GridMeta* M) {
     M->nlive = 0u;
     M->nfb = 0u;
     M->nfb2 = 0u;
+    M->nsig = 0u;
     M->bad = 0;
   }
 }
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(1024) k_grid_scan_top(const GridMeta* M, int* 
   }
 }
 
-__global__ void k_grid_scan_add(const GridMeta* M, int* start, int* cursor, const int* bsum) {
+__global__ void k_grid_scan_add(const GridMeta* M, int* start, int* cursor, const int* bsum,
+                                const unsigned* total) {
   if (M->bad) return;
   const int nc = M->ncell;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nc; i += gridDim.x * blockDim.x) {
@@ -285,11 +288,41 @@ __global__ void k_grid_scan_add(const GridMeta* M, int* start, int* cursor, cons
     if (i < nc) {
       v = start[i] + bsum[i / kScanItems];
     } else {
-      v = (int)M->nlive;  // start[ncell] = total
+      v = (int)*total;  // start[ncell] = total
     }
     start[i] = v;
     if (i < nc) cursor[i] = v;
   }
+}
+
+// signals in cell order: a warp's signals share cells (coherent shells,
+// cached cell ranges and units); non-finite signals go straight to the
+// exhaustive list
+__global__ void k_grid_sig_count(FindArgs a, GridMeta* M, int* sig_cell, int* scount,
+                                 int32_t* fb_list) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.m) return;
+  const double qx = a.sig[3 * j], qy = a.sig[3 * j + 1], qz = a.sig[3 * j + 2];
+  int c = -1;
+  if (!M->bad && isfinite(qx) && isfinite(qy) && isfinite(qz)) {
+    const int cx = cell_coord(qx, M->lo[0], M->inv_h, M->dim[0]);
+    const int cy = cell_coord(qy, M->lo[1], M->inv_h, M->dim[1]);
+    const int cz = cell_coord(qz, M->lo[2], M->inv_h, M->dim[2]);
+    c = (cz * M->dim[1] + cy) * M->dim[0] + cx;
+    atomicAdd(&scount[c], 1);
+    atomicAdd(&M->nsig, 1u);
+  } else {
+    fb_list[atomicAdd(&M->nfb, 1u)] = (int32_t)j;
+  }
+  sig_cell[j] = c;
+}
+
+__global__ void k_grid_sig_scatter(FindArgs a, const GridMeta* M, const int* sig_cell, int* scur,
+                                   int32_t* perm) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.m) return;
+  const int c = sig_cell[j];
+  if (c >= 0) perm[atomicAdd(&scur[c], 1)] = (int32_t)j;
 }
 
 __global__ void k_grid_scatter(FindArgs a, const GridMeta* M, const int* cell_of_row, int* cursor,
@@ -318,14 +351,11 @@ __device__ __forceinline__ void scan_cell(const int* start, const double4* gpos,
 
 __global__ void __launch_bounds__(256) k_grid_query(FindArgs a, const GridMeta* M,
                                                     const int* start, const double4* gpos,
-                                                    int32_t* fb_list) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.m) return;
+                                                    const int32_t* perm, int32_t* fb_list) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (M->bad || t >= (int64_t)M->nsig) return;
+  const int64_t j = perm[t];
   const double qx = a.sig[3 * j], qy = a.sig[3 * j + 1], qz = a.sig[3 * j + 2];
-  if (M->bad || !isfinite(qx) || !isfinite(qy) || !isfinite(qz)) {
-    fb_list[atomicAdd(&((GridMeta*)M)->nfb, 1u)] = (int32_t)j;
-    return;
-  }
   const int dx = M->dim[0], dy = M->dim[1], dz = M->dim[2];
   const double h = M->h, inv_h = M->inv_h, slack = M->slack;
   const double lx = M->lo[0], ly = M->lo[1], lz = M->lo[2];
@@ -432,7 +462,7 @@ void find_grid_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& 
   const size_t bsum_b = al(sizeof(int) * 2048);
   const size_t pos_b = al(sizeof(double4) * (size_t)cap);
   const size_t fb_b = al(sizeof(int32_t) * (size_t)a.m);
-  char* base = (char*)work.get(meta_b + row_b + 3 * cnt_b + bsum_b + pos_b + fb_b);
+  char* base = (char*)work.get(meta_b + row_b + 3 * cnt_b + bsum_b + pos_b + 3 * fb_b);
   GridMeta* M = (GridMeta*)base;
   int* cell_of_row = (int*)(base + meta_b);
   int* count = (int*)(base + meta_b + row_b);
@@ -441,6 +471,8 @@ void find_grid_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& 
   int* bsum = (int*)(base + meta_b + row_b + 3 * cnt_b);
   double4* gpos = (double4*)(base + meta_b + row_b + 3 * cnt_b + bsum_b);
   int32_t* fb = (int32_t*)(base + meta_b + row_b + 3 * cnt_b + bsum_b + pos_b);
+  int* sig_cell = (int*)(base + meta_b + row_b + 3 * cnt_b + bsum_b + pos_b + fb_b);
+  int32_t* perm = (int32_t*)(base + meta_b + row_b + 3 * cnt_b + bsum_b + pos_b + 2 * fb_b);
 
   const int rgrid = (int)std::min<int64_t>(4LL * ctx.sm_count, (cap + 255) / 256);
   const int cgrid = (int)std::min<int64_t>(4LL * ctx.sm_count, (max_cells + 256) / 256);
@@ -452,12 +484,21 @@ void find_grid_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& 
   k_grid_scan_blocks<<<(max_cells + kScanItems - 1) / kScanItems, 1024, 0, stream>>>(M, count,
                                                                                     start, bsum);
   k_grid_scan_top<<<1, 1024, 0, stream>>>(M, bsum);
-  k_grid_scan_add<<<cgrid, 256, 0, stream>>>(M, start, cursor, bsum);
+  k_grid_scan_add<<<cgrid, 256, 0, stream>>>(M, start, cursor, bsum, &M->nlive);
   k_grid_scatter<<<rgrid, 256, 0, stream>>>(a, M, cell_of_row, cursor, gpos);
-  k_grid_query<<<(unsigned)((a.m + 255) / 256), 256, 0, stream>>>(a, M, start, gpos, fb);
+  // signals in cell order (count -> scan -> scatter, reusing count/cursor)
+  const unsigned sgrid = (unsigned)((a.m + 255) / 256);
+  GS_CUDA(cudaMemsetAsync(count, 0, sizeof(int) * (size_t)max_cells, stream));
+  k_grid_sig_count<<<sgrid, 256, 0, stream>>>(a, M, sig_cell, count, fb);
+  k_grid_scan_blocks<<<(max_cells + kScanItems - 1) / kScanItems, 1024, 0, stream>>>(M, count,
+                                                                                    cursor, bsum);
+  k_grid_scan_top<<<1, 1024, 0, stream>>>(M, bsum);
+  k_grid_scan_add<<<cgrid, 256, 0, stream>>>(M, cursor, count, bsum, &M->nsig);
+  k_grid_sig_scatter<<<sgrid, 256, 0, stream>>>(a, M, sig_cell, count, perm);
+  k_grid_query<<<sgrid, 256, 0, stream>>>(a, M, start, gpos, perm, fb);
   k_grid_fallback<<<ctx.sm_count * 4, kGfThreads, 0, stream>>>(a, M, fb);
   GS_CUDA(cudaGetLastError());
-  g_launches += 10;
+  g_launches += 15;
   if (!ctx.d_fallbacks) GS_CUDA(cudaMalloc(&ctx.d_fallbacks, sizeof(unsigned long long)));
   GS_CUDA(cudaMemcpyAsync(ctx.d_fallbacks, &M->nfb, 2 * sizeof(unsigned), cudaMemcpyDeviceToDevice,
                           stream));

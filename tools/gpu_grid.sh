@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-m-sweep --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e']['ms_per_step']); print(json.dumps(d['find_microbench']['grid_lines'])[:900])"
+timeout 900 python -m pytest tests/test_gpu_grid_find.py tests/test_gpu_engine.py -x -q > gpurun_out/grid_tests.log 2>&1; echo "grid tests rc=$?"; tail -3 gpurun_out/grid_tests.log
+for mode in 4; do timeout 300 python tools/find_bench.py 1000000 10000 100000 1000000 --mode $mode --reps 5 | cut -c1-140; done
