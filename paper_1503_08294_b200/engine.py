@@ -58,7 +58,9 @@ def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, back
     the same device engine and matches the reference run bit for bit.
     ``checkpoints`` records (units, signals, sample_s, find_s, update_s,
     total_s) the first time the unit count reaches each value.  The
-    approximate hash-grid variant (use_grid=True, grid.py) is out of scope.
+    reference's hash grid (use_grid=True, grid.py:98-133) is approximate and
+    has no exact parity target; the exact device grid (GS_FIND_GRID) serves
+    the batched find, where its per-call build is amortised.
     """
     import ctypes as C
     import time
@@ -69,7 +71,8 @@ def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, back
 
     if use_grid:
         raise ValueError("the approximate hash-grid (indexed) variant is not provided; "
-                         "use_grid=False runs the exact single-signal engine")
+                         "use_grid=False runs the exact single-signal engine (the exact "
+                         "device grid serves batched finds: find_mode=FIND_GRID)")
     lib = _lib.load_library()
     p1 = replace(params, batch_floor=1, batch_cap=1)
     rng = np.random.Generator(np.random.Philox(seed))

@@ -7,3 +7,5 @@ ncu --set full --clock-control none --import-source on -k k_filter -c 1 -o gpuru
 ncu --set full --clock-control none --import-source on -k k_filter -c 1 -o gpurun_out/prof_filter_1e5 -f python tools/find_bench.py 1000000 100000 --reps 1 >> gpurun_out/ncu_filter.log 2>&1
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -s 6000 -c 1500 --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-find-microbench --no-m-sweep > gpurun_out/launches_bench.log 2>&1
 ls -la gpurun_out
+ncu --set full --clock-control none --import-source on -k regex:k_grid_query -c 1 -o gpurun_out/prof_grid_query -f python tools/find_bench.py 1000000 1000000 --mode 4 --reps 1 > gpurun_out/ncu_grid.log 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_grid.csv python tools/find_bench.py 1000000 10000 1000000 --mode 4 --reps 1 >> gpurun_out/ncu_grid.log 2>&1
