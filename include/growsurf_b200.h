@@ -181,8 +181,9 @@ gs_status gs_engine_resolve_host(gs_engine *eng, const double *signals, int64_t 
                                  const int64_t *win_b, const int64_t *win_s,
                                  const double *d_win, gs_batch_stats *out);
 /* Per-phase device time (CUDA events on the engine stream) accumulated over
- * synchronous steps: out[0] find ms, out[1] update ms.  enable: 1 on, 0 off,
- * -1 leave unchanged. */
+ * steps: out[0] find ms, out[1] update ms.  enable: 1 every batch, k > 1 one
+ * batch in k weighted by k (an estimate with the event records off the
+ * critical path), 0 off, -1 leave unchanged. */
 gs_status gs_engine_phase_ms(gs_engine *eng, int enable, double out[2]);
 /* Replace the run parameters used by subsequent updates (EngineParams). */
 gs_status gs_engine_set_params(gs_engine *eng, const gs_params *params);

@@ -870,6 +870,9 @@ struct gs_engine {
   cudaEvent_t ev[kEvRing][3] = {};
   int ev_head = 0, ev_count = 0;
   bool timing = false;
+  int timing_every = 1;      // time one batch in timing_every (weighted by it)
+  long long timing_seq = 0;
+  int ev_w[kEvRing] = {};
   double find_ms = 0.0, update_ms = 0.0;
   // host mirror of the last known counters
   int next_id = 0, n_edges = 0, n_units = 0;
@@ -1317,7 +1320,9 @@ extern "C" gs_status gs_engine_set_unit(gs_engine* e, int64_t id, const double* 
 }
 
 namespace {
-void harvest_timing(gs_engine* e);
+// fold the timing ring's oldest entries into find_ms / update_ms until at
+// most `keep` remain (waits only for the batches it folds)
+void harvest_timing(gs_engine* e, int keep = 0);
 
 // find + update for one batch on the engine stream.  With sig_idx the find
 // gathers the signals from the sampler's cloud into d_sig (fused sampling).
@@ -1327,10 +1332,16 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
   ensure_capacity(e, m, 3 * m);
   WinRec* rec = (WinRec*)e->rec_buf.get(sizeof(WinRec) * (size_t)m);
-  if (e->timing && e->ev_count == gs_engine::kEvRing) harvest_timing(e);  // ring full: sync
-  const bool timed = e->timing;
-  cudaEvent_t* evs = e->ev[(e->ev_head + e->ev_count) % gs_engine::kEvRing];
-  if (timed) GS_CUDA(cudaEventRecord(evs[0], e->stream));
+  // ring full: fold the older half, batches far behind the ones in flight
+  // (no stall of an asynchronous run)
+  if (e->timing && e->ev_count == gs_engine::kEvRing) harvest_timing(e, gs_engine::kEvRing / 2);
+  const bool timed = e->timing && (e->timing_seq++ % e->timing_every) == 0;
+  const int ev_slot = (e->ev_head + e->ev_count) % gs_engine::kEvRing;
+  cudaEvent_t* evs = e->ev[ev_slot];
+  if (timed) {
+    e->ev_w[ev_slot] = e->timing_every;
+    GS_CUDA(cudaEventRecord(evs[0], e->stream));
+  }
   launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
   if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
   launch_update(e, d_sig, rec, m);
@@ -1352,15 +1363,15 @@ extern "C" gs_status gs_engine_step_device(gs_engine* e, const double* d_sig, in
 }
 
 namespace {
-void harvest_timing(gs_engine* e) {
-  for (; e->ev_count > 0; --e->ev_count) {
+void harvest_timing(gs_engine* e, int keep) {
+  for (; e->ev_count > keep; --e->ev_count) {
     cudaEvent_t* evs = e->ev[e->ev_head];
     float a = 0.f, b = 0.f;
     GS_CUDA(cudaEventSynchronize(evs[2]));
     GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
     GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
-    e->find_ms += a;
-    e->update_ms += b;
+    e->find_ms += a * e->ev_w[e->ev_head];
+    e->update_ms += b * e->ev_w[e->ev_head];
     e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
   }
 }
@@ -1373,7 +1384,13 @@ extern "C" gs_status gs_engine_phase_ms(gs_engine* e, int enable, double out[2])
       for (auto& trio : e->ev)
         for (auto& ev : trio) GS_CUDA(cudaEventCreate(&ev));
     }
-    if (enable >= 0) e->timing = enable != 0;
+    // enable: 0 off, 1 every batch, k > 1 one batch in k (weighted by k: an
+    // estimate that keeps the per-batch event records off the critical path)
+    if (enable >= 0) {
+      e->timing = enable != 0;
+      e->timing_every = enable > 1 ? enable : 1;
+      e->timing_seq = 0;
+    }
     if (out) {
       out[0] = e->find_ms;
       out[1] = e->update_ms;

@@ -171,7 +171,7 @@ def step(net: Network, batch) -> _lib.GsBatchStats:
 def run_multi(source, params: EngineParams, seed: int, executor=None, *,
               variant: str = "multi-b200", dataset: str | None = None,
               find_mode: int = _lib.FIND_AUTO, capacity: int = 4096,
-              device_sampling: bool | None = None):
+              device_sampling: bool | None = None, phase_timing: bool = True):
     """Run the multi-signal engine to convergence or the signal cap.
 
     Same driver contract as multi.py:134-202: Philox(seed) stream, two seed
@@ -211,8 +211,10 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     edges = 0
     perf = time.perf_counter
     phase = np.zeros(2, np.float64)
-    if executor is None:
-        _lib.check(lib.gs_engine_phase_ms(net.handle, 1, phase))
+    if executor is None and phase_timing:
+        # find_s / update_s: with batches in flight, one batch in 16 is timed
+        # (per-batch event records would cost ~8 us of every batch)
+        _lib.check(lib.gs_engine_phase_ms(net.handle, 16 if lookahead else 1, phase))
     st = _lib.GsBatchStats()
     # fixed batch size + device sampling: the host enqueues batches ahead and
     # only polls for convergence (gs_engine_set_async); the device counts
