@@ -419,6 +419,63 @@ def m_sweep(lib, src, wparams, seed, ms=(256, 1024, 4096, 16384, 65536), budget_
     return out
 
 
+def other_configs(lib, names=("cfg1", "cfg2"), budget_s=20.0):
+    """BASELINE configs 1 and 2 (the SOAM runs the reference converges on):
+    time to converge from the two seed units with device sampling and the
+    asynchronous loop, CUDA events on the engine stream (same run as the
+    reference's, bit for bit: tests/test_gpu_engine.py golden runs)."""
+    import numpy as np
+    import torch
+
+    from paper_1503_08294_b200 import _lib, workloads
+    from paper_1503_08294_b200.device_sampling import DeviceCloudSampler
+    from paper_1503_08294_b200.network import Network
+
+    ref_note = {"cfg1": "reference: converges V=218 after 299,392 signals in 6.6 s on 1 core (SURVEY 8(d))",
+                "cfg2": "reference: converges V=681 after 4.28 M signals in 78.8 s on 8 cores (SURVEY 8(d))"}
+    out = {}
+    for name in names:
+        src, params, seed, desc = workloads.make(name)
+        m = params.batch_cap
+        pts_dev = torch.from_numpy(src.points).cuda()
+        rng = np.random.Generator(np.random.Philox(seed))
+        seeds = src.sample(rng, 2)
+        net = Network(params, capacity=8192)
+        net.reserve(8192)
+        net.set_async(8)
+        sampler = DeviceCloudSampler(None, rng, device_ptr=pts_dev.data_ptr(),
+                                     npts=src.points.shape[0])
+        for s_ in seeds:
+            net.add_unit(s_, params.theta0)
+        stream = torch.cuda.ExternalStream(net.stream_handle())
+        st = _lib.GsBatchStats()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        enq = 0
+        seq = C.c_int64()
+        while enq * m < params.max_signals:
+            _lib_check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
+            enq += 1
+            if enq % 4 == 0:
+                _lib_check(lib.gs_engine_stats_lagged(net.handle, 7, C.byref(st), C.byref(seq)))
+                if seq.value >= 0 and (st.converged or time.perf_counter() - t0 > budget_s):
+                    break
+        e1.record(stream)
+        _lib_check(lib.gs_engine_stats(net.handle, C.byref(st)))
+        sec = e0.elapsed_time(e1) * 1e-3
+        sig = int(st.batches) * m
+        out[name] = {"desc": desc, "m": m, "converged": bool(st.converged), "signals": sig,
+                     "batches": int(st.batches), "time_to_converge_s": sec,
+                     "signals_per_s": sig / sec, "units": int(st.units), "edges": int(st.edges),
+                     "reference": ref_note.get(name)}
+        sampler.close()
+        net.close()
+        del pts_dev
+    return out
+
+
 def _lib_check(rc):
     from paper_1503_08294_b200 import _lib
 
@@ -622,6 +679,9 @@ def run_b200_arm(args):
     sweep = None
     if rank == 0 and world == 1 and not args.no_m_sweep:
         sweep = m_sweep(lib, src, dict(workloads.WORKLOADS[args.workload]["params"]), seed)
+    others = None
+    if rank == 0 and world == 1 and not args.no_m_sweep:
+        others = other_configs(lib)
     fmb = None
     if rank == 0 and not args.no_find_microbench:
         fmb = find_microbench(lib, _lib.default_context(),
@@ -652,6 +712,7 @@ def run_b200_arm(args):
             "phase_ms_per_step": {"find": find_ms, "update": update_ms},
             "find_microbench": fmb,
             "m_sweep": sweep,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
