@@ -707,9 +707,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ long long s_ll32[33];
   __shared__ int s_cta[2][kCluster];
   __shared__ long long s_ctal[2][kCluster];
-  __shared__ int s_plist[kUpdThreads];  // this CTA's slice of the window's processed list
-  __shared__ unsigned char s_hblow[kUpdThreads];  // B: winner trained at its own time
-  __shared__ unsigned char s_abs[kUpdThreads];  // last_active absent at window start: b | s<<1
   __shared__ int s_walk[kWalkCap];  // units this CTA queued for replay
   __shared__ int s_nwalk;
   __shared__ int s_i[8];
@@ -753,6 +750,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   long long tick0 = 0, minla = 0;
   bool cand = false;
   int cb = -1;
+  bool my_proc = false;  // this thread's window signal is processed ...
+  int my_rank = 0, my_j = 0;  // ... at this rank
+  bool my_hblow = false;
+  int my_abs = 0;
   while (j0 < m) {
     if (lead) t_ph = clock64();
     if (!resume) {
@@ -782,25 +783,24 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       }
       minla = cl_min_ll(mla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
       if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
-      const bool proc = cand && S.firstwin[cb] == j;
-      const int rank = cl_excl_scan(proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
-      if (proc) {
-        int* dst = cmap(s_plist, rank / kUpdThreads);
-        dst[rank % kUpdThreads] = j;
-      }
-      csync();
+      // every thread keeps its own signal: its processing rank (batch
+      // order among the processed signals) is all the later phases need
+      my_proc = cand && S.firstwin[cb] == j;
+      my_rank = cl_excl_scan(my_proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
+      my_j = j;
       rbase = 0;
       if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
     }
     const long long next_sweep = c->next_sweep;
     const int n_units = c->n_units;
     const bool iso = c->iso_count > 0;
-    // ---- B: events and adapt_threshold outcomes; thread g owns rank g
+    // ---- B: events and adapt_threshold outcomes; each processed signal on
+    //      the thread that found it in A
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
-    int evr = 0x7fffffff;
-    if (g >= rbase && g < nproc) {
-      const int r = g;
-      const int jj = s_plist[tid];
+    long long evkey = 0x7fffffffffffffffLL;  // (rank << 32) | signal of this thread's event
+    if (my_proc && my_rank >= rbase) {
+      const int r = my_rank;
+      const int jj = my_j;
       const WinRec w = rec[jj];
       const int b = w.b, s = w.s;
       const long long tick_j = tick0 + r + 1;
@@ -855,35 +855,33 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (!found) ev = true;  // connect_or_reset creates b-s
       const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, kcn), P.c_b) < P.h_t;
       if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
-      s_hblow[tid] = hb_low ? 1 : 0;
+      my_hblow = hb_low;
       // last_active presence at the window start (dict order stamps)
-      s_abs[tid] = (unsigned char)((la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0));
-      if (ev) evr = r;
+      my_abs = (la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0);
+      if (ev) evkey = ((long long)r << 32) | (unsigned)jj;
     }
-    const int rstar = min(cl_min(evr, s_warp, s_cta, parity), nproc);
-    if (tid == 0) {
-      s_i[4] = rstar < nproc ? cmap(s_plist, rstar / kUpdThreads)[rstar % kUpdThreads]
-                             : wend;
-    }
-    __syncthreads();
-    const int jstar = s_i[4];
+    // the first event: smallest rank, and its signal, in one cluster reduction
+    const long long kmin = cl_min_ll(evkey, s_ll32, s_ctal, parity);
+    const bool has_ev = kmin != 0x7fffffffffffffffLL;
+    const int rstar = has_ev ? (int)(kmin >> 32) : nproc;
+    const int jstar = has_ev ? (int)(kmin & 0xffffffffLL) : wend;
     if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
     // ---- C1: claims, last_active (+ order stamps), patience/threshold,
     //      touched-unit owners, edge-age replay
-    const bool com = g >= rbase && g < rstar;
+    const bool com = my_proc && my_rank >= rbase && my_rank < rstar;
     WinRec cw;
     int cj = 0;
     if (com) {
-      cj = s_plist[tid];
+      cj = my_j;
       cw = rec[cj];
-      const long long ctick = tick0 + g + 1;
-      const int absent = s_abs[tid];
+      const long long ctick = tick0 + my_rank + 1;
+      const int absent = my_abs;
       S.claim[cw.b] = batch_no;
       if (absent & 1) atomicMin(&S.la_stamp[cw.b], 3 * ctick);
       if (absent & 2) atomicMin(&S.la_stamp[cw.s], 3 * ctick + 1);
       atomicMax(&S.la_val[cw.b], ctick);
       atomicMax(&S.la_val[cw.s], ctick);
-      const int p = adapt_outcome(S, P, cw.b, cj, s_hblow[tid] != 0);
+      const int p = adapt_outcome(S, P, cw.b, cj, my_hblow);
       if (p != -2) {
         S.patience[cw.b] = p & 0x3fffffff;
         if (p >> 30) S.theta[cw.b] = dmul(S.theta[cw.b], P.rho);
