@@ -1095,10 +1095,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         j0 = jstar + 1;
       }
     } else {
+      // no event: every candidate's winner had its first signal committed,
+      // so reset (before its barrier) already cleared every firstwin entry
+      // of this window -- the next window may start without another barrier
       if (lead) c->discarded += (wend - j0) - nproc;
-      if (cand) S.firstwin[cb] = kNone32;
       resume = false;
       j0 = wend;
+      continue;
     }
     if (!resume) csync();  // firstwin cleared before the next window's candidates
   }
