@@ -925,10 +925,18 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     csync();
     if (lead) { const long long t_ = clock64(); acc[3] += t_ - t_ph; t_ph = t_; }
     // ---- C2: each touched unit's position / habituation sequence replayed once
+    // (the walker clears its unit's touched mark: no phase reads it until C1)
     const int nloc = min(s_nwalk, kWalkCap);
-    for (int i = tid; i < nloc; i += kUpdThreads) walk_unit(S, P, sig, s_walk[i], jstar);
+    for (int i = tid; i < nloc; i += kUpdThreads) {
+      walk_unit(S, P, sig, s_walk[i], jstar);
+      S.touchfirst[s_walk[i]] = kNone32;
+    }
     const int nglob = c->nwalk;  // overflow list (only for very high degrees)
-    for (int i = g; i < nglob; i += kWinC) walk_unit(S, P, sig, (int)S.scratch[i], jstar);
+    for (int i = g; i < nglob; i += kWinC) {
+      walk_unit(S, P, sig, (int)S.scratch[i], jstar);
+      S.touchfirst[(int)S.scratch[i]] = kNone32;
+    }
+    const int deaths0 = c->deaths;  // stable until the event path
     csync();
     if (lead) { const long long t_ = clock64(); acc[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
@@ -944,10 +952,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       c->next_sweep = ns;
     }
     if (com) S.firstwin[cw.b] = kNone32;
-    const int deaths0 = c->deaths;  // stable until the event path (read before its barrier)
-    for (int i = tid; i < nloc; i += kUpdThreads) S.touchfirst[s_walk[i]] = kNone32;
-    for (int i = g; i < nglob; i += kWinC) S.touchfirst[(int)S.scratch[i]] = kNone32;
-    csync();
+    // the event path reads neither firstwin nor the walked units' marks, and
+    // its own barrier publishes these clears; only a next window that starts
+    // right away needs them first
+    if (rstar == nproc && wend < m) csync();
     if (tid == 0) s_nwalk = 0;
     if (lead) {
       c->nwalk = 0;
