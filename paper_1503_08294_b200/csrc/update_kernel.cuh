@@ -629,13 +629,6 @@ __device__ __forceinline__ int crank_of() {
   }
 }
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
-constexpr int kWalkCap = 6 * kUpdThreads;      // per-CTA replay queue (overflow: global)
-
-__device__ __forceinline__ void push_walk(const DevState& S, int* s_walk, int* s_nwalk, int u) {
-  const int k = atomicAdd(s_nwalk, 1);
-  if (k < kWalkCap) s_walk[k] = u;
-  else S.scratch[atomicAdd(&S.cnt->nwalk, 1)] = u;
-}
 
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
 // used with alternating parity so a CTA running one call ahead cannot
@@ -707,8 +700,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ long long s_ll32[33];
   __shared__ int s_cta[2][kCluster];
   __shared__ long long s_ctal[2][kCluster];
-  __shared__ int s_walk[kWalkCap];  // units this CTA queued for replay
-  __shared__ int s_nwalk;
   __shared__ int s_i[8];
   __shared__ int s_over[kMaxDeg];
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
@@ -736,7 +727,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->stale_n = 0;
     c->nwalk = 0;
   }
-  if (tid == 0) s_nwalk = 0;
   csync();
   int j0 = 0;
   // A window [j0, wend) is evaluated once (A: candidates, scan: processed
@@ -886,20 +876,16 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         S.patience[cw.b] = p & 0x3fffffff;
         if (p >> 30) S.theta[cw.b] = dmul(S.theta[cw.b], P.rho);
       }
-      // the first thread to touch a unit queues it for one replay (any thread
-      // may own it: the replay order comes from firstwin, not from the owner)
-      if (atomicExch(&S.touchfirst[cw.b], 1) == kNone32) push_walk(S, s_walk, &s_nwalk, cw.b);
       const int db = S.deg[cw.b];
       const int2* B = S.adj + (size_t)cw.b * kMaxDeg;
       for (int c0 = 0; c0 < db; c0 += kStage) {
         const int dc = min(kStage, db - c0);
         int2 nb[kStage];
         stage_adj(B + c0, dc, nb);
-        int tf[kStage], jv[kStage], age[kStage];
+        int jv[kStage], age[kStage];
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
           if (k < dc) {
-            tf[k] = atomicExch(&S.touchfirst[nb[k].x], 1);
             jv[k] = S.firstwin[nb[k].x];
             age[k] = S.eage[nb[k].y];
           }
@@ -913,7 +899,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
           if (k >= dc) continue;
-          if (tf[k] == kNone32) push_walk(S, s_walk, &s_nwalk, nb[k].x);
           if (jv[k] < jstar && jv[k] > cj) continue;  // v's own signal replays this edge
           int a = age[k];
           if (jv[k] < cj) a = (sv[k] == cw.b) ? 0 : a + 1;
@@ -924,18 +909,12 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
     csync();
     if (lead) { const long long t_ = clock64(); acc[3] += t_ - t_ph; t_ph = t_; }
-    // ---- C2: each touched unit's position / habituation sequence replayed once
-    // (the walker clears its unit's touched mark: no phase reads it until C1)
-    const int nloc = min(s_nwalk, kWalkCap);
-    for (int i = tid; i < nloc; i += kUpdThreads) {
-      walk_unit(S, P, sig, s_walk[i], jstar);
-      S.touchfirst[s_walk[i]] = kNone32;
-    }
-    const int nglob = c->nwalk;  // overflow list (only for very high degrees)
-    for (int i = g; i < nglob; i += kWinC) {
-      walk_unit(S, P, sig, (int)S.scratch[i], jstar);
-      S.touchfirst[(int)S.scratch[i]] = kNone32;
-    }
+    // ---- C2: each touched unit's position / habituation sequence replayed
+    //      once, over every unit slot: a unit no committed signal touched has
+    //      no replay key (its own and its neighbours' firstwin) and keeps its
+    //      values, so no touched list (nor the atomics to build one) is needed
+    const int nid = c->next_id;
+    for (int u = g; u < nid; u += kWinC) walk_unit(S, P, sig, u, jstar);
     const int deaths0 = c->deaths;  // stable until the event path
     csync();
     if (lead) { const long long t_ = clock64(); acc[6] += t_ - t_ph; t_ph = t_; }
@@ -956,9 +935,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // its own barrier publishes these clears; only a next window that starts
     // right away needs them first
     if (rstar == nproc && wend < m) csync();
-    if (tid == 0) s_nwalk = 0;
     if (lead) {
-      c->nwalk = 0;
       const long long t_ = clock64();
       acc[7] += t_ - t_ph;
       t_ph = t_;
