@@ -186,6 +186,12 @@ struct FindArgs {
   const double* rowpos = nullptr;
   const int* rowpos_n = nullptr;
   int64_t rowpos_stride = 0;
+  // engine: FP32 unit pairs of the same snapshot (valid with rowpos), their
+  // centre and max-norm bound (the screened small find copies them)
+  const float4* rowf = nullptr;
+  int64_t rowf_stride = 0;
+  const double* fcen = nullptr;
+  const unsigned* fpm_bits = nullptr;
   const double* sig = nullptr;   // m x 3 f64
   // optional fused sampling: signal j is sig_pts[sig_idx[j]] and the find
   // writes it to sig (then non-const) for the update that follows

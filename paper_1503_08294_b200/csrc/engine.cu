@@ -102,6 +102,11 @@ struct Counters {
   long long ev_cutoff;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
+  // FP32 unit pairs of the row snapshot (the screened find's staging): centre
+  // (row 0 rounded to FP32) and max-norm of P' = fl32(p - centre), float bits
+  double fcen[3];
+  unsigned fpm_bits;
+  int pad_;
 };
 
 struct Params {
@@ -127,6 +132,7 @@ struct DevState {
   int32_t* iso_pos;     // index in iso_list or -1
   int32_t* rows;        // row -> id (append-only, id order)
   double* rowpos;       // [3][U] row-ordered positions (dead rows +inf) for the find
+  float4* rowf;         // [2][rowf_stride] FP32 unit pairs of the same rows (A0, A1)
   int32_t* eage;        // [EC]
   int32_t* efree;       // [EC] free edge-id stack
   int32_t* iso_list;    // isolated units (network.py:93 _isolated)
@@ -137,6 +143,7 @@ struct DevState {
   Counters* cnt;
   gs_batch_stats* stats;
   int U, EC;
+  int rowf_stride;  // unit pairs per half of rowf (multiple of 64)
 };
 
 // ---------------------------------------------------------------------------
@@ -927,6 +934,9 @@ void grow_units(gs_engine* e, int new_u) {
   grow_array(S.rows, old, new_u, st);
   dfree(S.rowpos, st);  // regenerated by the next update (stride U)
   S.rowpos = (double*)dmalloc(sizeof(double) * 3 * (size_t)new_u, st);
+  dfree(S.rowf, st);
+  S.rowf_stride = ((new_u + 1) / 2 + 63) / 64 * 64;
+  S.rowf = (float4*)dmalloc(sizeof(float4) * 2 * (size_t)S.rowf_stride, st);
   {
     const int stale = -1;
     GS_CUDA(cudaMemcpyAsync(&S.cnt->rowpos_n, &stale, sizeof(int), cudaMemcpyHostToDevice, st));
@@ -1094,6 +1104,10 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   a.rowpos = e->S.rowpos;
   a.rowpos_n = &e->S.cnt->rowpos_n;
   a.rowpos_stride = e->U;
+  a.rowf = e->S.rowf;
+  a.rowf_stride = e->S.rowf_stride;
+  a.fcen = e->S.cnt->fcen;
+  a.fpm_bits = &e->S.cnt->fpm_bits;
   a.sig = d_sig + 3 * lo;
   a.sig_idx = sig_idx ? sig_idx + lo : nullptr;
   a.sig_pts = sig_pts;
@@ -1192,7 +1206,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
-                  S.rowpos};
+                  S.rowpos, S.rowf};
   for (void* q : ptrs) dfree(q, e->stream);  // stream is idle: back to the pool at once
   hfree(e->h_stats);
   hfree(e->h_ring);

@@ -333,72 +333,87 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
   bool full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
   if (!full_scan) {
     const int nr = (int)n;
-    // centre: row 0 rounded to FP32 (any centre is valid; the bound uses Pmax)
     double cx = 0.0, cy = 0.0, cz = 0.0;
-    if (nr > 0) {
-      double x, y, z;
-      if (sf_row(a, compact, 0, x, y, z) && fabs(x) < 1e30 && fabs(y) < 1e30 && fabs(z) < 1e30) {
-        cx = (double)__double2float_rn(x);
-        cy = (double)__double2float_rn(y);
-        cz = (double)__double2float_rn(z);
-      }
-    }
-    // stage the FP32 unit pairs; max-norm of P' for Pmax.  Four pairs per
-    // thread per step with every load issued before any use (one memory
-    // latency per step, not one per row).
     float pm = 0.f;
-    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-    for (int p0 = threadIdx.x; p0 < npad; p0 += 4 * kSfThreads) {
-      double X[8], Y[8], Z[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const int r = 2 * (p0 + (t >> 1) * kSfThreads) + (t & 1);
-        X[t] = Y[t] = Z[t] = kInf;
-        if (r < nr) {
-          if (compact) {
-            X[t] = a.rowpos[r];
-            Y[t] = a.rowpos[a.rowpos_stride + r];
-            Z[t] = a.rowpos[2 * a.rowpos_stride + r];
-          } else if (!load_row(a, r, X[t], Y[t], Z[t])) {
-            X[t] = kInf;
-          }
+    if (compact && a.rowf) {
+      // the update kernel left these rows as FP32 unit pairs (same centre
+      // rule, same bound): a coalesced copy
+      cx = a.fcen[0];
+      cy = a.fcen[1];
+      cz = a.fcen[2];
+      pm = __uint_as_float(*a.fpm_bits);
+      const int np64c = (((nr + 1) / 2) + 63) & ~63;
+      for (int p = threadIdx.x; p < np64c; p += kSfThreads) {
+        A0[p] = a.rowf[p];
+        A1[p] = a.rowf[a.rowf_stride + p];
+      }
+      __syncthreads();
+    } else {
+      // centre: row 0 rounded to FP32 (any centre is valid; the bound uses Pmax)
+      if (nr > 0) {
+        double x, y, z;
+        if (sf_row(a, compact, 0, x, y, z) && fabs(x) < 1e30 && fabs(y) < 1e30 && fabs(z) < 1e30) {
+          cx = (double)__double2float_rn(x);
+          cy = (double)__double2float_rn(y);
+          cz = (double)__double2float_rn(z);
         }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int p = p0 + q * kSfThreads;
-        if (p >= npad) break;
-        float ax[2], ay[2], az[2], w[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double x = X[2 * q + h], y = Y[2 * q + h], z = Z[2 * q + h];
-          ax[h] = ay[h] = az[h] = 0.f;
-          w[h] = INFINITY;
-          // a row with a non-finite coordinate has d2 = inf or NaN for every
-          // signal and is never selected (nor are dead rows, +inf here and
-          // in the update's row snapshot): it is left out like a dead one
-          if (isfinite(x) && isfinite(y) && isfinite(z)) {
-            const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
-                        pz = __double2float_rn(z - cz);
-            ax[h] = -2.f * px;
-            ay[h] = -2.f * py;
-            az[h] = -2.f * pz;
-            w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
-            const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
-            pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
+      // stage the FP32 unit pairs; max-norm of P' for Pmax.  Four pairs per
+      // thread per step with every load issued before any use (one memory
+      // latency per step, not one per row).
+      const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+      for (int p0 = threadIdx.x; p0 < npad; p0 += 4 * kSfThreads) {
+        double X[8], Y[8], Z[8];
+  #pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int r = 2 * (p0 + (t >> 1) * kSfThreads) + (t & 1);
+          X[t] = Y[t] = Z[t] = kInf;
+          if (r < nr) {
+            if (compact) {
+              X[t] = a.rowpos[r];
+              Y[t] = a.rowpos[a.rowpos_stride + r];
+              Z[t] = a.rowpos[2 * a.rowpos_stride + r];
+            } else if (!load_row(a, r, X[t], Y[t], Z[t])) {
+              X[t] = kInf;
+            }
           }
         }
-        A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
-        A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+  #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int p = p0 + q * kSfThreads;
+          if (p >= npad) break;
+          float ax[2], ay[2], az[2], w[2];
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double x = X[2 * q + h], y = Y[2 * q + h], z = Z[2 * q + h];
+            ax[h] = ay[h] = az[h] = 0.f;
+            w[h] = INFINITY;
+            // a row with a non-finite coordinate has d2 = inf or NaN for every
+            // signal and is never selected (nor are dead rows, +inf here and
+            // in the update's row snapshot): it is left out like a dead one
+            if (isfinite(x) && isfinite(y) && isfinite(z)) {
+              const float px = __double2float_rn(x - cx), py = __double2float_rn(y - cy),
+                          pz = __double2float_rn(z - cz);
+              ax[h] = -2.f * px;
+              ay[h] = -2.f * py;
+              az[h] = -2.f * pz;
+              w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
+              const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+              pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
+            }
+          }
+          A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
+          A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+        }
       }
+  #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+      if (lane == 0) s_pm[warp] = pm;
+      __syncthreads();
+      pm = s_pm[0];
+  #pragma unroll
+      for (int k = 1; k < kSfWarps; ++k) pm = fmaxf(pm, s_pm[k]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
-    if (lane == 0) s_pm[warp] = pm;
-    __syncthreads();
-    pm = s_pm[0];
-#pragma unroll
-    for (int k = 1; k < kSfWarps; ++k) pm = fmaxf(pm, s_pm[k]);
     // |p - c| <= sqrt(3) * max_k |P'_k| / (1 - u), rounded up generously
     const double pmax = (double)pm * 1.7320508075688774 * (1.0 + 1e-6);
 

@@ -726,6 +726,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->inserted_start = c->next_id;
     c->stale_n = 0;
     c->nwalk = 0;
+    c->fpm_bits = 0u;
   }
   csync();
   int j0 = 0;
@@ -1092,23 +1093,65 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   }
   {
     // row-ordered positions for the next find (its staging becomes coalesced
-    // copies instead of a gather through rows); every CTA takes a slice
+    // copies instead of a gather through rows), and the same rows as the
+    // screened find's FP32 unit pairs {-2P'x, -2P'y, -2P'z, |P'|^2} relative
+    // to row 0 rounded to FP32 (dead or non-finite rows: +inf, left out of
+    // the max-norm bound); every CTA takes a slice of the pairs
     const int n = c->nrows;
     const size_t U = (size_t)S.U;
-    for (int r0 = 0; r0 < n; r0 += 2 * kWinC) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = r0 + q * kWinC + g;
-        if (r < n) {
-          const int u = S.rows[r];
-          double4 p = make_double4(INFINITY, INFINITY, INFINITY, 0.0);
-          if (S.alive[u]) p = S.pos[u];
-          S.rowpos[r] = p.x;
-          S.rowpos[U + r] = p.y;
-          S.rowpos[2 * U + r] = p.z;
+    double cx = 0.0, cy = 0.0, cz = 0.0;
+    if (n > 0) {
+      const int u0 = S.rows[0];
+      if (S.alive[u0]) {
+        const double4 p0 = S.pos[u0];
+        if (fabs(p0.x) < 1e30 && fabs(p0.y) < 1e30 && fabs(p0.z) < 1e30) {
+          cx = (double)__double2float_rn(p0.x);
+          cy = (double)__double2float_rn(p0.y);
+          cz = (double)__double2float_rn(p0.z);
         }
       }
     }
+    if (lead) {
+      c->fcen[0] = cx;
+      c->fcen[1] = cy;
+      c->fcen[2] = cz;
+    }
+    const int np64 = (((n + 1) / 2) + 63) & ~63;
+    float4* A0 = S.rowf;
+    float4* A1 = S.rowf + S.rowf_stride;
+    float pm = 0.f;
+    for (int p = g; p < np64; p += kWinC) {
+      float ax[2], ay[2], az[2], w[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 2 * p + h;
+        ax[h] = ay[h] = az[h] = 0.f;
+        w[h] = INFINITY;
+        if (r < n) {
+          const int u = S.rows[r];
+          double4 q = make_double4(INFINITY, INFINITY, INFINITY, 0.0);
+          if (S.alive[u]) q = S.pos[u];
+          S.rowpos[r] = q.x;
+          S.rowpos[U + r] = q.y;
+          S.rowpos[2 * U + r] = q.z;
+          if (isfinite(q.x) && isfinite(q.y) && isfinite(q.z)) {
+            const float px = __double2float_rn(q.x - cx), py = __double2float_rn(q.y - cy),
+                        pz = __double2float_rn(q.z - cz);
+            ax[h] = -2.f * px;
+            ay[h] = -2.f * py;
+            az[h] = -2.f * pz;
+            w[h] = __double2float_rn((double)px * px + (double)py * py + (double)pz * pz);
+            const float mn = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+            pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;
+          }
+        }
+      }
+      A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
+      A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits, __float_as_uint(pm));
   }
   if (crank != 0) return;
   if (tid == 0) c->rowpos_n = c->nrows;
