@@ -888,7 +888,23 @@ struct gs_engine {
   // asynchronous sampled runs draw the indices of async_depth batches per
   // sampler launch (fixed batch size)
   int64_t pf_m = 0, pf_next = 0, pf_left = 0;
+  // ... on a side stream, one group ahead, into two halves of idx_buf, so a
+  // group's draws overlap the previous group's update kernels (16 SMs busy)
+  cudaStream_t side = nullptr;
+  cudaEvent_t pf_done[2] = {}, use_done[2] = {};
+  int64_t pf_issued = 0, pf_used = 0;
+  int pf_half = 0;
 };
+
+namespace {
+// drop prefetched groups (the side stream is drained first: its sampler
+// launches advance the sampler state)
+void drop_prefetch(gs_engine* e) {
+  if (e->side) GS_CUDA(cudaStreamSynchronize(e->side));
+  e->pf_left = e->pf_next = 0;
+  e->pf_issued = e->pf_used = 0;
+}
+}  // namespace
 
 namespace {
 
@@ -1221,6 +1237,14 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   e->sig_buf.release();
   e->rec_buf.release();
   e->idx_buf.release();
+  if (e->side) {
+    cudaStreamSynchronize(e->side);
+    cudaStreamDestroy(e->side);
+  }
+  for (int h = 0; h < 2; ++h) {
+    if (e->pf_done[h]) cudaEventDestroy(e->pf_done[h]);
+    if (e->use_done[h]) cudaEventDestroy(e->use_done[h]);
+  }
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -1422,6 +1446,7 @@ extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
   return guarded([&] {
     GS_CHECK(e, GS_VALUE_ERROR, "null engine");
     GS_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->side) GS_CUDA(cudaStreamSynchronize(e->side));  // sampler state settled
     latest_stats(e);
     harvest_timing(e);
     check_stats(e);
@@ -1475,18 +1500,42 @@ extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64
       // one sampler launch draws the next async_depth batches (same stream
       // order as one launch per batch); a batch-size change would reorder
       // draws already taken, so it is an error while some remain
-      GS_CHECK(e->pf_left == 0 || e->pf_m == m, GS_VALUE_ERROR,
+      GS_CHECK(e->pf_issued == 0 || e->pf_m == m, GS_VALUE_ERROR,
                "asynchronous sampled runs need a fixed batch size");
+      const int64_t k = e->async_depth;
       if (e->pf_left == 0) {
-        const int64_t k = e->async_depth;
-        int64_t* ring = (int64_t*)e->idx_buf.get(sizeof(int64_t) * (size_t)(k * m));
-        sampler_indices(smp, k * m, ring, e->stream);
-        e->launches++;
+        if (!e->side) {
+          GS_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+          for (int h = 0; h < 2; ++h) {
+            GS_CUDA(cudaEventCreateWithFlags(&e->pf_done[h], cudaEventDisableTiming));
+            GS_CUDA(cudaEventCreateWithFlags(&e->use_done[h], cudaEventDisableTiming));
+          }
+        }
+        if (e->pf_issued == 0) {
+          // first group: its buffers must be ready on the side stream too
+          GS_CUDA(cudaStreamSynchronize(e->stream));
+          e->idx_buf.get(sizeof(int64_t) * (size_t)(2 * k * m));
+          GS_CUDA(cudaStreamSynchronize(e->stream));
+        }
+        int64_t* base = (int64_t*)e->idx_buf.p;
+        auto issue = [&](int64_t grp) {
+          const int h = (int)(grp & 1);
+          if (grp >= 2) GS_CUDA(cudaStreamWaitEvent(e->side, e->use_done[h], 0));
+          sampler_indices(smp, k * m, base + (size_t)h * k * m, e->side);
+          GS_CUDA(cudaEventRecord(e->pf_done[h], e->side));
+          e->launches++;
+          e->pf_issued++;
+        };
+        if (e->pf_issued == 0) issue(0);
+        const int64_t G = e->pf_used++;
+        e->pf_half = (int)(G & 1);
+        GS_CUDA(cudaStreamWaitEvent(e->stream, e->pf_done[e->pf_half], 0));
+        issue(G + 1);  // next group's draws overlap this group's batches
         e->pf_m = m;
         e->pf_next = 0;
         e->pf_left = k;
       }
-      d_idx = (int64_t*)e->idx_buf.p + e->pf_next * m;
+      d_idx = (int64_t*)e->idx_buf.p + ((size_t)e->pf_half * k + e->pf_next) * m;
       e->pf_next++;
       e->pf_left--;
     } else {
@@ -1495,6 +1544,8 @@ extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64
       e->launches++;
     }
     step_device_impl(e, d_sig, m, d_idx, sampler_points(smp));
+    if (e->async_depth > 0 && e->pf_left == 0)  // this half may be refilled now
+      GS_CUDA(cudaEventRecord(e->use_done[e->pf_half], e->stream));
     if (out) {
       GS_CUDA(cudaStreamSynchronize(e->stream));
       latest_stats(e);
@@ -1602,7 +1653,7 @@ extern "C" gs_status gs_engine_set_async(gs_engine* e, int depth) {
   return guarded([&] {
     GS_CHECK(e && depth >= 0 && depth <= 1024, GS_VALUE_ERROR, "bad async depth");
     e->async_depth = depth;
-    e->pf_left = e->pf_next = 0;  // prefetched indices (if any) are dropped
+    drop_prefetch(e);  // prefetched indices (if any) are dropped
     // {halt_on_converge, halted}: leaving async mode also clears the halt, so
     // the network can be stepped further like the reference's
     const int flags[2] = {depth > 0 ? 1 : 0, 0};
@@ -1636,7 +1687,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     GS_CUDA(cudaMemsetAsync(S.stats, 0, sizeof(gs_batch_stats), st));
     GS_CUDA(cudaStreamSynchronize(st));
     e->next_id = e->n_edges = e->n_units = 0;
-    e->pf_left = e->pf_next = 0;
+    drop_prefetch(e);
     e->reset_seq = e->issued;
     memset(e->h_stats, 0, sizeof(gs_batch_stats));
     harvest_timing(e);
