@@ -1088,7 +1088,8 @@ long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
   return e->h_res[0];
 }
 
-void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m) {
+void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m,
+                   gs_batch_stats* st_out = nullptr) {
   if constexpr (kCluster > 8) {  // clusters beyond the portable 8 CTAs need an opt-in
     static bool opted = false;
     if (!opted) {
@@ -1097,7 +1098,8 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
     }
   }
   e->batch_no++;
-  k_update_batch<<<kCluster, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m, e->batch_no);
+  k_update_batch<<<kCluster, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m,
+                                                          e->batch_no, st_out ? st_out : e->S.stats);
   GS_CUDA(cudaGetLastError());
   e->launches++;
   ++g_launches;
@@ -1382,14 +1384,14 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   }
   launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
   if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
-  launch_update(e, d_sig, rec, m);
+  // the kernel writes its stats straight into the host ring slot (pinned,
+  // mapped under UVA): no copy between this batch's kernels and the next
+  const int slot = (int)(e->issued % gs_engine::kEvRing);
+  launch_update(e, d_sig, rec, m, e->h_ring + slot);
   if (timed) {
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;
   }
-  const int slot = (int)(e->issued % gs_engine::kEvRing);
-  GS_CUDA(cudaMemcpyAsync(e->h_ring + slot, e->S.stats, sizeof(gs_batch_stats),
-                          cudaMemcpyDeviceToHost, e->stream));
   GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
   e->issued++;
   e->ring_latest = true;

@@ -695,7 +695,8 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 #endif
 __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     k_update_batch(DevState S, Params P, const double* __restrict__ sig,
-                   const WinRec* __restrict__ rec, int m, int batch_no) {
+                   const WinRec* __restrict__ rec, int m, int batch_no,
+                   gs_batch_stats* st_out) {
   __shared__ int s_warp[33];
   __shared__ long long s_ll32[33];
   __shared__ int s_cta[2][kCluster];
@@ -713,7 +714,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const bool lead = crank == 0 && tid == 0;
   const int warp = tid >> 5, lane = tid & 31;
   int parity = 0;
-  if (S.cnt->halted) return;  // converged earlier in an asynchronous run (uniform)
+  if (S.cnt->halted) {  // converged earlier in an asynchronous run (uniform)
+    // the batch's stats slot still gets the (unchanged) latest values
+    if (st_out != S.stats && threadIdx.x == 0 && crank_of() == 0) {
+      *st_out = *S.stats;
+      __threadfence_system();
+    }
+    return;
+  }
   const long long t_kernel = clock64();
   long long t_ph = t_kernel;
   // the lead thread's phase timers stay in registers until the kernel ends
@@ -1208,5 +1216,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     st->batches = c->batches;
     st->halted = c->halted;
     for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
+    // the host's ring slot (pinned, mapped): no copy between the kernels
+    if (st_out != st) {
+      *st_out = *st;
+      __threadfence_system();
+    }
   }
 }
