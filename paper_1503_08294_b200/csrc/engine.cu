@@ -880,6 +880,10 @@ struct gs_engine {
   int timing_every = 1;      // time one batch in timing_every (weighted by it)
   long long timing_seq = 0;
   int ev_w[kEvRing] = {};
+  int64_t ev_b[kEvRing] = {};  // batch (issue index) a timing entry belongs to
+  // completion events for the stats ring: one batch in kStatEvery (the
+  // lagged reader rounds down to the nearest one)
+  static constexpr int kStatEvery = 4;
   double find_ms = 0.0, update_ms = 0.0;
   // host mirror of the last known counters
   int next_id = 0, n_edges = 0, n_units = 0;
@@ -1380,6 +1384,7 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   cudaEvent_t* evs = e->ev[ev_slot];
   if (timed) {
     e->ev_w[ev_slot] = e->timing_every;
+    e->ev_b[ev_slot] = e->issued;
     GS_CUDA(cudaEventRecord(evs[0], e->stream));
   }
   launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
@@ -1392,7 +1397,8 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;
   }
-  GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
+  if (e->issued % gs_engine::kStatEvery == 0)
+    GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
   e->issued++;
   e->ring_latest = true;
 }
@@ -1464,21 +1470,22 @@ extern "C" gs_status gs_engine_stats_lagged(gs_engine* e, int64_t lag, gs_batch_
   return guarded([&] {
     GS_CHECK(e && out && lag >= 0 && lag < gs_engine::kEvRing - 1, GS_VALUE_ERROR,
              "lag must be in [0, 63)");
-    const int64_t target = e->issued - 1 - lag;
+    int64_t target = e->issued - 1 - lag;
+    target -= target % gs_engine::kStatEvery;  // the nearest batch with a completion event
     if (seq) *seq = target < e->reset_seq ? -1 : target - e->reset_seq;
     if (target < e->reset_seq) {
       memset(out, 0, sizeof(*out));
       return;
     }
     GS_CUDA(cudaEventSynchronize(e->stat_ev[target % gs_engine::kEvRing]));
-    // per-phase timings of the batches known complete
-    while (e->ev_count > 0 && (int64_t)e->ev_count > lag) {
+    // per-phase timings of the batches known complete (up to target)
+    while (e->ev_count > 0 && e->ev_b[e->ev_head] <= target) {
       cudaEvent_t* evs = e->ev[e->ev_head];
       float a = 0.f, b = 0.f;
       GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
       GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
-      e->find_ms += a;
-      e->update_ms += b;
+      e->find_ms += a * e->ev_w[e->ev_head];
+      e->update_ms += b * e->ev_w[e->ev_head];
       e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
       e->ev_count--;
     }
