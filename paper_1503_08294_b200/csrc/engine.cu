@@ -1102,8 +1102,17 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
     }
   }
   e->batch_no++;
-  k_update_batch<<<kCluster, kUpdThreads, 0, e->stream>>>(e->S, e->P, d_sig, d_rec, (int)m,
-                                                          e->batch_no, st_out ? st_out : e->S.stats);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kCluster);
+  cfg.blockDim = dim3(kUpdThreads);
+  cfg.stream = e->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GS_CUDA(cudaLaunchKernelEx(&cfg, k_update_batch, e->S, e->P, d_sig, d_rec, (int)m, e->batch_no,
+                             st_out ? st_out : e->S.stats));
   GS_CUDA(cudaGetLastError());
   e->launches++;
   ++g_launches;

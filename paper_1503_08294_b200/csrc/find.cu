@@ -306,6 +306,9 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
   const int npad = tile_rows / 2;  // unit pairs (tile_rows is a multiple of 128)
   float4* A0 = s_u;
   float4* A1 = s_u + npad;
+  // launched as a programmatic dependent of the previous kernel (the update):
+  // every CTA may already be resident; wait for that grid's results here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t sig0 = ((int64_t)blockIdx.x * kSfWarps + warp) * kFS;
@@ -615,12 +618,24 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
       fs = (a.m * 100 >= 170 * warps * 4 * sms) ? 4 : (a.m * 100 >= 170 * warps * 2 * sms) ? 2 : 1;
     }
     const unsigned grid = (unsigned)((a.m + warps * fs - 1) / (warps * fs));
+    // programmatic dependent launch: the CTAs become resident while the
+    // previous kernel (the 16-SM update) still runs and wait in-kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kSfThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (fs == 4)
-      find_small_f32_kernel<4><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<4>, a, tile_rows));
     else if (fs == 2)
-      find_small_f32_kernel<2><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<2>, a, tile_rows));
     else
-      find_small_f32_kernel<1><<<grid, kSfThreads, smem, stream>>>(a, tile_rows);
+      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<1>, a, tile_rows));
     GS_CUDA(cudaGetLastError());
     ++g_launches;
     return;

@@ -714,6 +714,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const bool lead = crank == 0 && tid == 0;
   const int warp = tid >> 5, lane = tid & 31;
   int parity = 0;
+  // programmatic dependent launch after the find: wait for its records
+  // here; the next batch's find may launch at once (its CTAs wait in turn)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (S.cnt->halted) {  // converged earlier in an asynchronous run (uniform)
     // the batch's stats slot still gets the (unchanged) latest values
     if (st_out != S.stats && threadIdx.x == 0 && crank_of() == 0) {
