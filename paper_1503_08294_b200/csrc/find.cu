@@ -309,6 +309,9 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
   // launched as a programmatic dependent of the previous kernel (the update):
   // every CTA may already be resident; wait for that grid's results here
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ... and let the update (16 SMs) become resident on the SMs this grid
+  // leaves free; it waits for this grid's records in turn
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t sig0 = ((int64_t)blockIdx.x * kSfWarps + warp) * kFS;

@@ -212,9 +212,9 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     perf = time.perf_counter
     phase = np.zeros(2, np.float64)
     if executor is None and phase_timing:
-        # find_s / update_s: with batches in flight, one batch in 16 is timed
+        # find_s / update_s: with batches in flight, one batch in 64 is timed
         # (per-batch event records would cost ~8 us of every batch)
-        _lib.check(lib.gs_engine_phase_ms(net.handle, 16 if lookahead else 1, phase))
+        _lib.check(lib.gs_engine_phase_ms(net.handle, 64 if lookahead else 1, phase))
     st = _lib.GsBatchStats()
     # fixed batch size + device sampling: the host enqueues batches ahead and
     # only polls for convergence (gs_engine_set_async); the device counts
