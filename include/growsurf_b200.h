@@ -190,9 +190,10 @@ gs_status gs_engine_set_params(gs_engine *eng, const gs_params *params);
 /* Synchronise the engine stream and copy out the last batch's stats. */
 gs_status gs_engine_stats(gs_engine *eng, gs_batch_stats *out);
 /* Stats of a device step at least `lag` steps before the newest one (0 <= lag
- * < 63; rounded down to a multiple of 4, the steps that carry a completion
- * event), waiting only for that step so later ones keep the GPU busy; *seq
- * receives its index (-1 and zeroed stats when fewer were issued). */
+ * < 63; the nearest earlier step that carries a completion event: every
+ * step, or in asynchronous sampled runs the last of each group), waiting only
+ * for that step so later ones keep the GPU busy; *seq receives its index
+ * (-1 and zeroed stats when none is available yet). */
 gs_status gs_engine_stats_lagged(gs_engine *eng, int64_t lag, gs_batch_stats *out, int64_t *seq);
 /* The engine's CUDA stream (cudaStream_t) for callers sharing it. */
 void *gs_engine_stream(gs_engine *eng);

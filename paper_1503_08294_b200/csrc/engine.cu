@@ -881,9 +881,8 @@ struct gs_engine {
   long long timing_seq = 0;
   int ev_w[kEvRing] = {};
   int64_t ev_b[kEvRing] = {};  // batch (issue index) a timing entry belongs to
-  // completion events for the stats ring: one batch in kStatEvery (the
-  // lagged reader rounds down to the nearest one)
-  static constexpr int kStatEvery = 4;
+  // batch (issue index) whose completion event a stats-ring slot holds
+  int64_t stat_batch[kEvRing];
   double find_ms = 0.0, update_ms = 0.0;
   // host mirror of the last known counters
   int next_id = 0, n_edges = 0, n_units = 0;
@@ -1215,6 +1214,7 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
       e->h_ring = (gs_batch_stats*)hmalloc(sizeof(gs_batch_stats) * gs_engine::kEvRing);
       memset(e->h_ring, 0, sizeof(gs_batch_stats) * gs_engine::kEvRing);
       for (auto& ev : e->stat_ev) GS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      for (auto& b : e->stat_batch) b = -1;
       e->d_res = (long long*)dmalloc(4 * sizeof(long long), st);
       e->h_res = (long long*)hmalloc(4 * sizeof(long long));
       const int64_t cap = std::max<int64_t>(1024, std::min<int64_t>(capacity_hint, 1 << 28));
@@ -1380,7 +1380,9 @@ void harvest_timing(gs_engine* e, int keep = 0);
 // find + update for one batch on the engine stream.  With sig_idx the find
 // gathers the signals from the sampler's cloud into d_sig (fused sampling).
 void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_t* sig_idx,
-                      const double* sig_pts) {
+                      const double* sig_pts, bool mark);
+void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_t* sig_idx,
+                      const double* sig_pts, bool mark = true) {
   GS_CHECK(e && d_sig && m > 0, GS_VALUE_ERROR, "bad step arguments");
   GS_CHECK(m < (1LL << 30), GS_VALUE_ERROR, "batch too large");
   ensure_capacity(e, m, 3 * m);
@@ -1406,8 +1408,12 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;
   }
-  if (e->issued % gs_engine::kStatEvery == 0)
+  // completion events only where the caller wants them (each one sits
+  // between two kernels and stops the programmatic overlap there)
+  if (mark) {
     GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
+    e->stat_batch[slot] = e->issued;
+  }
   e->issued++;
   e->ring_latest = true;
 }
@@ -1480,7 +1486,12 @@ extern "C" gs_status gs_engine_stats_lagged(gs_engine* e, int64_t lag, gs_batch_
     GS_CHECK(e && out && lag >= 0 && lag < gs_engine::kEvRing - 1, GS_VALUE_ERROR,
              "lag must be in [0, 63)");
     int64_t target = e->issued - 1 - lag;
-    target -= target % gs_engine::kStatEvery;  // the nearest batch with a completion event
+    // the nearest earlier batch that carries a completion event
+    while (target >= e->reset_seq && target > e->issued - gs_engine::kEvRing &&
+           e->stat_batch[target % gs_engine::kEvRing] != target)
+      --target;
+    if (target >= 0 && e->stat_batch[target % gs_engine::kEvRing] != target)
+      target = e->reset_seq - 1;  // none in reach: report "not yet"
     if (seq) *seq = target < e->reset_seq ? -1 : target - e->reset_seq;
     if (target < e->reset_seq) {
       memset(out, 0, sizeof(*out));
@@ -1561,7 +1572,10 @@ extern "C" gs_status gs_engine_step_sampled(gs_engine* e, gs_sampler* smp, int64
       sampler_indices(smp, m, d_idx, e->stream);
       e->launches++;
     }
-    step_device_impl(e, d_sig, m, d_idx, sampler_points(smp));
+    // asynchronous groups: one completion event per group, at its end (where
+    // the next group's draws break the kernel chain anyway)
+    step_device_impl(e, d_sig, m, d_idx, sampler_points(smp),
+                     e->async_depth == 0 || e->pf_left == 0);
     if (e->async_depth > 0 && e->pf_left == 0)  // this half may be refilled now
       GS_CUDA(cudaEventRecord(e->use_done[e->pf_half], e->stream));
     if (out) {
