@@ -629,7 +629,7 @@ def run_b200_arm(args):
                 "work": f"{per_sig:.0f} B per processed signal (winner + {mean_deg:.2f} neighbours: "
                         "pos+hab read/write, adjacency, edge ages, record, signal)",
                 "share_of_step": update_ms / (find_ms + update_ms),
-                "note": "sequential-semantics update on one CTA: latency-bound, not bandwidth-bound"}
+                "note": "sequential-semantics update on one 16-CTA cluster: bound by dependent L2 round trips and cluster barriers, not by bandwidth"}
 
     # e2e through the public API: host sampling + H2D per batch + stats D2H
     e2e = None
