@@ -167,9 +167,12 @@ gs_status gs_engine_step(gs_engine *eng, const double *signals, int64_t m, gs_ba
  * the engine's pinned stats block; read them with gs_engine_stats. */
 gs_status gs_engine_step_device(gs_engine *eng, const double *d_signals, int64_t m);
 /* Find only: writes device winner records for signals [lo, hi) of a device
- * batch (a multi-GPU shard), then gs_engine_update_device applies the full
- * batch's records (after an all-gather). Records are 32 bytes per signal:
- * int32 row1, int32 row2, float64 d2_1, float64 d2_2, 8 bytes padding. */
+ * batch (a multi-GPU shard) at record index lo.., then gs_engine_update_device
+ * applies the full batch's records (after an all-gather).  Records are
+ * GS_WINREC_BYTES = 16 bytes per signal: int32 winner ID, int32 second ID
+ * (ids, not rows: snapshot.ids[row], multi.py:72-78), float64 d_winner =
+ * sqrt(d2_1) correctly rounded. */
+#define GS_WINREC_BYTES 16
 gs_status gs_engine_find_device(gs_engine *eng, const double *d_signals, int64_t lo, int64_t hi,
                                 void *d_records);
 gs_status gs_engine_update_device(gs_engine *eng, const double *d_signals, int64_t m,
@@ -220,6 +223,21 @@ gs_status gs_engine_counts(gs_engine *eng, int64_t out[11]);
 gs_status gs_engine_export_units(gs_engine *eng, int64_t cap, int64_t *ids, double *pos,
                                  double *hab, double *theta, int64_t *ring, int64_t *patience,
                                  int64_t *last_active, int64_t *n_out);
+/* RunState (engine.py:101-119) over ids [0, next_id): *n_ids = next_id; when
+ * cap >= next_id, patience[u], last_active[u] (-1 = no entry) and stamp[u]
+ * (dict insertion order of the last_active entries; -1 = no entry) are
+ * written (any array may be NULL).  Replaces reading state.tick /
+ * state.next_sweep / state.patience / state.last_active. */
+gs_status gs_engine_get_run_state(gs_engine *eng, int64_t *tick, int64_t *next_sweep, int64_t cap,
+                                  int64_t *patience, int64_t *last_active, int64_t *stamp,
+                                  int64_t *n_ids);
+/* Load a RunState for the following updates (a fresh RunState() is tick 0,
+ * next_sweep 1024, n 0).  Ids [0, n) take patience / last_active (-1 = no
+ * entry) / stamp; stamps order the entries like dict insertion and must be
+ * < 3 * (tick + 1).  Ids [n, next_id) get no entry; n <= next_id. */
+gs_status gs_engine_set_run_state(gs_engine *eng, int64_t tick, int64_t next_sweep, int64_t n,
+                                  const int64_t *patience, const int64_t *last_active,
+                                  const int64_t *stamp);
 /* All edges (a, b, age), a < b, sorted (network.py:152-161). */
 gs_status gs_engine_export_edges(gs_engine *eng, int64_t cap, int64_t *abage, int64_t *n_out);
 /* Device audit (Network.audit, network.py:485-526): recomputes rings, degree

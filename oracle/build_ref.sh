@@ -16,6 +16,9 @@ cp -r "$src" "$tmp/pkg"
 rm -rf "$here/_ref"
 python -m pip install --quiet --no-index --no-build-isolation --no-deps \
   --find-links /opt/wheelhouse --target "$here/_ref" "$tmp/pkg"
+# the reference's own test suite travels with it (tests/test_ref_dropin.py runs
+# it with the B200 kernels registered as the default backend)
+cp -r "$src/tests" "$here/_ref/ref_tests"
 python - "$here/_ref" <<'PY'
 import sys
 sys.path.insert(0, sys.argv[1])

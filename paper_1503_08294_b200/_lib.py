@@ -95,6 +95,9 @@ _SIGNATURES = {
     "gs_engine_export_units": (C.c_int, [_vp, C.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                          C.POINTER(C.c_int64)]),
     "gs_engine_export_edges": (C.c_int, [_vp, C.c_int64, _vp, C.POINTER(C.c_int64)]),
+    "gs_engine_get_run_state": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                          C.c_int64, _vp, _vp, _vp, C.POINTER(C.c_int64)]),
+    "gs_engine_set_run_state": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp]),
     "gs_engine_audit": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
     "gs_sampler_create": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.POINTER(_vp)]),
     "gs_sampler_destroy": (None, [_vp]),

@@ -174,6 +174,7 @@ struct WinRec {
   int32_t b, s;
   double dwin;
 };
+static_assert(sizeof(WinRec) == GS_WINREC_BYTES, "WinRec layout is part of the C ABI");
 
 struct FindArgs {
   const double* pos = nullptr;   // plain rows: n x 3 f64

@@ -1799,6 +1799,77 @@ extern "C" gs_status gs_engine_export_units(gs_engine* e, int64_t cap, int64_t* 
   });
 }
 
+// RunState (engine.py:101-119) as arrays over ids [0, next_id): patience,
+// last_active (-1 absent) and the dict-order stamp of each last_active entry.
+extern "C" gs_status gs_engine_get_run_state(gs_engine* e, int64_t* tick, int64_t* next_sweep,
+                                             int64_t cap, int64_t* patience,
+                                             int64_t* last_active, int64_t* stamp,
+                                             int64_t* n_ids) {
+  return guarded([&] {
+    GS_CHECK(e && tick && next_sweep && n_ids, GS_VALUE_ERROR, "null argument");
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    const size_t n = (size_t)hc.next_id;
+    *tick = hc.tick;
+    *next_sweep = hc.next_sweep;
+    *n_ids = (int64_t)n;
+    if (cap < (int64_t)n) return;
+    cudaStream_t st = e->stream;
+    auto pt = d2h(e->S.patience, n, st);
+    auto la = d2h(e->S.la_val, n, st);
+    auto sp = d2h(e->S.la_stamp, n, st);
+    GS_CUDA(cudaStreamSynchronize(st));
+    for (size_t u = 0; u < n; ++u) {
+      if (patience) patience[u] = pt[u];
+      if (last_active) last_active[u] = la[u];
+      if (stamp) stamp[u] = la[u] == -1 ? -1 : sp[u];
+    }
+  });
+}
+
+// Load a RunState: ids [0, n) take the given values, ids [n, next_id) become
+// absent.  Stamps order the last_active entries (dict insertion order) and
+// must be < 3 * (tick + 1) so later entries sort after them.
+extern "C" gs_status gs_engine_set_run_state(gs_engine* e, int64_t tick, int64_t next_sweep,
+                                             int64_t n, const int64_t* patience,
+                                             const int64_t* last_active, const int64_t* stamp) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CHECK(tick >= 0 && n >= 0, GS_VALUE_ERROR, "bad run state");
+    GS_CHECK(n == 0 || (patience && last_active && stamp), GS_VALUE_ERROR, "null argument");
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    GS_CHECK(n <= hc.next_id, GS_VALUE_ERROR, "run state names an id that was never created");
+    const size_t N = (size_t)hc.next_id;
+    std::vector<int32_t> pt(N, 0);
+    std::vector<long long> la(N, -1), sp(N, kNone64);
+    for (int64_t u = 0; u < n; ++u) {
+      GS_CHECK(patience[u] >= 0 && patience[u] < (1LL << 31), GS_VALUE_ERROR, "bad patience");
+      GS_CHECK(last_active[u] >= -1, GS_VALUE_ERROR, "bad last_active");
+      pt[u] = (int32_t)patience[u];
+      if (last_active[u] != -1) {
+        GS_CHECK(stamp[u] < 3 * (tick + 1), GS_VALUE_ERROR, "bad last_active order stamp");
+        la[u] = last_active[u];
+        sp[u] = stamp[u];
+      }
+    }
+    cudaStream_t st = e->stream;
+    if (N) {
+      GS_CUDA(cudaMemcpyAsync(e->S.patience, pt.data(), sizeof(int32_t) * N,
+                              cudaMemcpyHostToDevice, st));
+      GS_CUDA(cudaMemcpyAsync(e->S.la_val, la.data(), sizeof(long long) * N,
+                              cudaMemcpyHostToDevice, st));
+      GS_CUDA(cudaMemcpyAsync(e->S.la_stamp, sp.data(), sizeof(long long) * N,
+                              cudaMemcpyHostToDevice, st));
+    }
+    const long long clocks[2] = {tick, next_sweep};
+    GS_CUDA(cudaMemcpyAsync(&e->S.cnt->tick, clocks, sizeof(clocks), cudaMemcpyHostToDevice, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 extern "C" gs_status gs_engine_export_edges(gs_engine* e, int64_t cap, int64_t* abage,
                                             int64_t* n_out) {
   return guarded([&] {

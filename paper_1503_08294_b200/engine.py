@@ -20,23 +20,27 @@ __all__ = ["find_winners_exhaustive", "update_single", "is_converged", "RunState
 
 
 def find_winners_exhaustive(snapshot: Snapshot, signal, backend=None) -> WinnerResult:
-    """engine.py:149-158 on the B200 scan."""
+    """engine.py:149-158 on the B200 scan (or on ``backend``, a kernel-backend
+    module, when given)."""
     n = len(snapshot)
     if n < 2:
         raise StateError(f"need at least 2 units to find winners, have {n}")
     pos = np.ascontiguousarray(snapshot.positions, dtype=np.float64)
-    r1, r2, d1, d2 = kernels.best_two_single(pos, n, float(signal[0]), float(signal[1]),
-                                             float(signal[2]))
+    kb = kernels if backend is None else backend
+    r1, r2, d1, d2 = kb.best_two_single(pos, n, float(signal[0]), float(signal[1]),
+                                        float(signal[2]))
     ids = snapshot.ids
     return WinnerResult(int(ids[r1]), int(ids[r2]), math.sqrt(d1), math.sqrt(d2))
 
 
 def update_single(net: Network, params: EngineParams, signal, wr: WinnerResult,
                   state: RunState | None = None, grid=None) -> None:
-    """engine.py:283-355: one full update for one signal."""
+    """engine.py:283-355: one full update for one signal; ``state=None`` is a
+    fresh RunState (engine.py:301-302)."""
     if not (net.is_alive(wr.winner) and net.is_alive(wr.second)):
         raise StateError(f"stale winner result ({wr.winner}, {wr.second})")
-    resolve_and_update(net, params, np.asarray(signal, dtype=np.float64).reshape(1, 3), [wr])
+    resolve_and_update(net, params, np.asarray(signal, dtype=np.float64).reshape(1, 3), [wr],
+                       state, grid)
 
 
 def is_converged(net: Network, params: EngineParams) -> bool:

@@ -41,7 +41,9 @@ def _floats(path, no, text, what):
     try:
         return [float(f) for f in fields]
     except ValueError:
-        raise ParseError(path, no, f"bad {what} coordinates: {text!r}") from None
+        # sampling.py:243 (OFF vertices) / :283 (XYZ points)
+        bad = "bad vertex coordinates" if what == "vertex" else "bad coordinates"
+        raise ParseError(path, no, f"{bad}: {text!r}") from None
 
 
 def load_off(path):

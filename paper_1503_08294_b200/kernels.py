@@ -26,6 +26,9 @@ __all__ = ["best_two_single", "scan_best_two_into", "NAME"]
 
 NAME = "b200"
 
+# calls served so far (evidence that a registry lookup really reached the B200)
+calls = {"best_two_single": 0, "scan_best_two_into": 0}
+
 
 def _as_pos(pos):
     pos = np.asarray(pos)
@@ -39,6 +42,7 @@ def best_two_single(pos, n, x, y, z):
     pos = _as_pos(pos)
     lib = _lib.load_library()
     ctx = _lib.default_context()
+    calls["best_two_single"] += 1
     r1, r2 = C.c_int64(), C.c_int64()
     d1, d2 = C.c_double(), C.c_double()
     _lib.check(lib.gs_best_two_single(ctx.handle, pos, pos.shape[0], int(n), float(x), float(y),
@@ -61,6 +65,7 @@ def scan_best_two_into(pos, n, signals, out_idx, out_d2, tile):
             raise ValueError("outputs must be writable C-contiguous (>=m, 2) arrays")
     lib = _lib.load_library()
     ctx = _lib.default_context()
+    calls["scan_best_two_into"] += 1
     _lib.check(lib.gs_scan_best_two_into(ctx.handle, pos, pos.shape[0], int(n), signals,
                                          signals.shape[0], out_idx, out_idx.shape[0], out_d2,
                                          out_d2.shape[0], int(tile)))

@@ -46,14 +46,85 @@ __all__ = [
 ]
 
 
+_SWEEP_EVERY = 1024  # engine.py:98
+
+
+class _Patience(dict):
+    """``state.patience`` read back from the device: a missing key reads as 0
+    (the device keeps one counter per id, where the reference's dict may hold
+    an explicit 0; ``patience.get(u, 0)``, engine.py:234, is the same)."""
+
+    def __missing__(self, key):
+        return 0
+
+
 class RunState:
-    """Placeholder for API compatibility: the run state (tick, patience,
-    last_active, sweep clock) lives on the device inside the Network."""
+    """Cross-update bookkeeping for one run (engine.py:101-119).
 
-    __slots__ = ()
+    Same fields as the reference: ``patience`` (id -> consecutive stuck
+    wins), ``last_active`` (id -> tick of the last top-two appearance, in
+    dict insertion order: the sweep removes stale units in that order),
+    ``tick`` and ``next_sweep``.  The device keeps the live copy inside the
+    Network; ``resolve_and_update`` / ``update_single`` load this object
+    into the device before the updates and write the device's values back
+    into it afterwards, so a caller that passes one RunState across calls
+    sees the reference's values, and ``state=None`` is a fresh RunState per
+    call, as in the reference (multi.py:114-115, engine.py:301-302).
+    """
+
+    __slots__ = ("patience", "last_active", "tick", "next_sweep")
+
+    def __init__(self):
+        self.patience: dict[int, int] = _Patience()
+        self.last_active: dict[int, int] = {}
+        self.tick = 0
+        self.next_sweep = _SWEEP_EVERY
 
 
-def _scan_batch(snapshot: Snapshot, signals, tile: int | None = None):
+def _load_run_state(net: Network, state: RunState) -> None:
+    """Copy a host RunState into the device network (gs_engine_set_run_state)."""
+    keys = [int(u) for u in list(state.patience) + list(state.last_active)]
+    if any(u < 0 for u in keys):
+        raise ValueError("run state names a negative unit id")
+    n = max(keys) + 1 if keys else 0
+    patience = np.zeros(n, np.int64)
+    last_active = np.full(n, -1, np.int64)
+    stamp = np.full(n, -1, np.int64)
+    for u, c in state.patience.items():
+        patience[int(u)] = int(c)
+    k = len(state.last_active)
+    for i, (u, t) in enumerate(state.last_active.items()):
+        last_active[int(u)] = int(t)
+        stamp[int(u)] = i - k  # before every entry the device creates later
+    _lib.check(_lib.load_library().gs_engine_set_run_state(
+        net.handle, int(state.tick), int(state.next_sweep), n, patience.ctypes.data,
+        last_active.ctypes.data, stamp.ctypes.data))
+
+
+def _store_run_state(net: Network, state: RunState) -> None:
+    """Write the device run state back into ``state`` (gs_engine_get_run_state)."""
+    lib = _lib.load_library()
+    tick, nsw, n = C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.check(lib.gs_engine_get_run_state(net.handle, C.byref(tick), C.byref(nsw), 0, None,
+                                           None, None, C.byref(n)))
+    patience = np.zeros(n.value, np.int64)
+    last_active = np.zeros(n.value, np.int64)
+    stamp = np.zeros(n.value, np.int64)
+    _lib.check(lib.gs_engine_get_run_state(net.handle, C.byref(tick), C.byref(nsw), n.value,
+                                           patience.ctypes.data, last_active.ctypes.data,
+                                           stamp.ctypes.data, C.byref(n)))
+    state.tick = int(tick.value)
+    state.next_sweep = int(nsw.value)
+    pt = _Patience()
+    for u in np.flatnonzero(patience).tolist():
+        pt[u] = int(patience[u])
+    state.patience = pt
+    have = np.flatnonzero(last_active != -1)
+    order = have[np.argsort(stamp[have], kind="stable")]
+    state.last_active = {int(u): int(last_active[u]) for u in order.tolist()}
+
+
+def _scan_batch(snapshot: Snapshot, signals, tile: int | None = None, backend=None):
     n = len(snapshot)
     if n < 2:
         raise StateError(f"need at least 2 units to find winners, have {n}")
@@ -61,8 +132,9 @@ def _scan_batch(snapshot: Snapshot, signals, tile: int | None = None):
     m = signals.shape[0]
     out_idx = np.empty((m, 2), dtype=np.int64)
     out_d2 = np.empty((m, 2), dtype=np.float64)
-    kernels.scan_best_two_into(np.ascontiguousarray(snapshot.positions, dtype=np.float64), n,
-                               signals, out_idx, out_d2, n if tile is None else tile)
+    kb = kernels if backend is None else backend
+    kb.scan_best_two_into(np.ascontiguousarray(snapshot.positions, dtype=np.float64), n,
+                          signals, out_idx, out_d2, n if tile is None else tile)
     return out_idx, out_d2
 
 
@@ -77,7 +149,7 @@ def _to_results(snapshot: Snapshot, out_idx, out_d2) -> list[WinnerResult]:
 def batch_find_winners(snapshot: Snapshot, batch, backend=None,
                        tile: int | None = None) -> list[WinnerResult]:
     """Winner pair for every signal, computed on the B200 (multi.py:81-87)."""
-    out_idx, out_d2 = _scan_batch(snapshot, batch, tile)
+    out_idx, out_d2 = _scan_batch(snapshot, batch, tile, backend)
     return _to_results(snapshot, out_idx, out_d2)
 
 
@@ -90,7 +162,20 @@ def b200_executor(tile: int | None = None):
     return execute
 
 
-sequential_executor = b200_executor
+def sequential_executor(backend=None, tile: int | None = None):
+    """multi.py:90-96: ``execute(snapshot, batch)`` over one batched scan.
+
+    ``backend`` is a kernel-backend module (``best_two_single`` /
+    ``scan_best_two_into``, kernels/__init__.py:6-7); None is this
+    package's B200 kernels (the reference's default is its compiled scan).
+    """
+    if backend is None:
+        return b200_executor(tile=tile)
+
+    def execute(snapshot: Snapshot, batch) -> list[WinnerResult]:
+        return batch_find_winners(snapshot, batch, backend=backend, tile=tile)
+
+    return execute
 
 
 @dataclass(frozen=True)
@@ -116,9 +201,11 @@ class ExecConfig:
 
 def parallel_batch_find_winners(snapshot: Snapshot, batch, cfg: ExecConfig | None = None,
                                 backend=None) -> list[WinnerResult]:
-    """parallel.py:91-97 on the B200 scan."""
+    """parallel.py:91-97 on the B200 scan (one launch covers every worker's
+    slice; a foreign ``backend`` gets the whole batch in one call, which its
+    contract makes identical to the sliced calls)."""
     cfg = cfg or ExecConfig()
-    return batch_find_winners(snapshot, batch, tile=cfg.tile)
+    return batch_find_winners(snapshot, batch, backend=backend, tile=cfg.tile)
 
 
 def timed_find(snapshot: Snapshot, batch, cfg: ExecConfig | None = None, backend=None):
@@ -130,7 +217,12 @@ def timed_find(snapshot: Snapshot, batch, cfg: ExecConfig | None = None, backend
 
 def parallel_executor(cfg: ExecConfig | None = None, backend=None):
     """parallel.py:107-114 equivalent: the parallelism is the GPU's."""
-    return b200_executor(tile=(cfg or ExecConfig()).tile)
+    cfg = cfg or ExecConfig()
+
+    def execute(snapshot: Snapshot, batch) -> list[WinnerResult]:
+        return parallel_batch_find_winners(snapshot, batch, cfg, backend=backend)
+
+    return execute
 
 
 def _winner_arrays(winners):
@@ -147,14 +239,24 @@ def _winner_arrays(winners):
 
 def resolve_and_update(net: Network, params: EngineParams, batch, winners,
                        state: RunState | None = None, grid=None) -> BatchOutcome:
-    """Winner lock + batch-order update on the device (multi.py:99-131)."""
+    """Winner lock + batch-order update on the device (multi.py:99-131).
+
+    ``state`` is the run's RunState; None is a fresh one for this call
+    (multi.py:114-115).  ``grid`` is accepted for signature compatibility:
+    the device find keeps no incremental index to relocate.
+    """
     net.set_params(params)
     batch = np.ascontiguousarray(batch, dtype=np.float64).reshape(-1, 3)
     b, s, d = _winner_arrays(winners)
+    if batch.shape[0] != b.shape[0]:
+        raise ValueError(f"{batch.shape[0]} signals but {b.shape[0]} winner results")
+    _load_run_state(net, state if state is not None else RunState())
     st = _lib.GsBatchStats()
     _lib.check(_lib.load_library().gs_engine_resolve_host(net.handle, batch, batch.shape[0], b, s,
                                                           d, C.byref(st)))
     net._touch()
+    if state is not None:
+        _store_run_state(net, state)
     return BatchOutcome(int(st.processed), int(st.discarded), int(st.inserted))
 
 

@@ -9,8 +9,11 @@ to the host (cached until the next mutation); mutators run the serial
 device primitives.  The training loop itself (run_multi /
 resolve_and_update in multi.py) never leaves the device.
 
-Deviation: ``state_arrays()`` returns host COPIES (device memory cannot be
-aliased by numpy); write habituation/positions with ``set_unit``.
+``state_arrays()`` returns host copies whose element writes go through to
+the device (``hab[:] = 0.05``, ``pos[rows] = moved``, ``theta[k] *= rho``,
+the in-place edits the reference's tests make on its live views,
+network.py:178-186); a write that cannot be intercepted (a slice of a view,
+``np.copyto``) fails loudly on a read-only array instead of being lost.
 """
 
 from __future__ import annotations
@@ -49,6 +52,65 @@ def to_gs_params(params: EngineParams, find_mode: int = _lib.FIND_AUTO) -> _lib.
         params.eps_b, params.eps_n, params.theta0, int(params.max_age), params.tau_b,
         params.tau_n, params.h_t, params.rho, int(params.ring_patience),
         int(bool(params.allow_boundary)), int(find_mode), int(params.stale_factor))
+
+
+class _WriteThrough(np.ndarray):
+    """Host copy of one device unit array (positions, habituation or
+    thresholds, id order) that writes changed rows back to the device.
+
+    The buffer is read-only: ``__setitem__`` and the in-place operators
+    (``+=``, ``*=`` ... via ``__array_ufunc__`` with ``out=self``) are the
+    only writers, and both push every changed row with ``set_unit``.
+    Slices and ufunc results are plain ndarrays (slices stay read-only).
+    """
+
+    def __new__(cls, data, net, field):
+        obj = np.array(data, copy=True).view(cls)
+        obj._gs = (net, field)
+        obj.flags.writeable = False
+        return obj
+
+    def __array_finalize__(self, obj):
+        self._gs = None
+
+    def __getitem__(self, key):
+        return np.ndarray.__getitem__(self.view(np.ndarray), key)
+
+    def _commit(self, before):
+        net, field = self._gs
+        now = self.view(np.ndarray)
+        diff = now.view(np.uint64) != before.view(np.uint64)
+        if diff.ndim == 2:
+            diff = diff.any(axis=1)
+        ids = net._mirror()["ids"].copy()
+        for r in np.flatnonzero(diff).tolist():
+            kw = {"position": now[r]} if field == "pos" else {field: float(now[r])}
+            net.set_unit(int(ids[r]), **kw)
+
+    def _write(self, fn):
+        if self._gs is None:
+            raise ValueError("assignment destination is read-only")
+        before = self.view(np.ndarray).copy()
+        self.flags.writeable = True
+        try:
+            fn(self.view(np.ndarray))
+        finally:
+            self.flags.writeable = False
+        self._commit(before)
+
+    def __setitem__(self, key, value):
+        self._write(lambda a: a.__setitem__(key, value))
+
+    def __array_ufunc__(self, ufunc, method, *inputs, out=None, **kw):
+        plain = tuple(x.view(np.ndarray) if isinstance(x, _WriteThrough) else x for x in inputs)
+        if out is None:
+            return getattr(ufunc, method)(*plain, **kw)
+        targets = [o for o in out if isinstance(o, _WriteThrough)]
+        if len(targets) != 1 or len(out) != 1 or method != "__call__":
+            raise ValueError("assignment destination is read-only")
+        result = getattr(ufunc, method)(*plain, **kw)
+        targets[0]._write(lambda a: a.__setitem__(Ellipsis, result))
+        return targets[0]
 
 
 class Network:
@@ -243,8 +305,15 @@ class Network:
         return float(np.max(hab))
 
     def state_arrays(self):
+        """(ids, positions, habituation, thresholds) in id order
+        (network.py:178-186).  ids is read-only; the other three write
+        element edits through to the device (see _WriteThrough)."""
         m = self._mirror()
-        return m["ids"].copy(), m["pos"].copy(), m["hab"].copy(), m["theta"].copy()
+        ids = m["ids"].copy()
+        ids.flags.writeable = False
+        return (ids, _WriteThrough(m["pos"], self, "pos"),
+                _WriteThrough(m["hab"], self, "habituation"),
+                _WriteThrough(m["theta"], self, "threshold"))
 
     def row_of(self, unit_id: int) -> int:
         return self._require(unit_id)

@@ -48,6 +48,13 @@ CASES = {
                      params=dict(theta0=0.3, allow_boundary=True, max_signals=150_000)),
     "paper_rule": dict(source=("cloud", "torus100k"), seed=21,
                        params=dict(theta0=0.15, max_signals=200_000)),
+    # V > 4096 (tests/golden/make_golden.py): AUTO crosses the screened small
+    # find, the n <= 6144 FP64 small find and the grid
+    "v8k": dict(source=("cloud", "torus100k"), seed=7,
+                params=dict(theta0=0.05, batch_cap=8192, max_signals=1_500_000)),
+    "v8k_fixed": dict(source=("cloud", "torus100k"), seed=7,
+                      params=dict(theta0=0.05, batch_floor=8192, batch_cap=8192,
+                                  max_signals=1_228_800)),
 }
 
 
@@ -81,7 +88,7 @@ def run_device_trace(name, find_mode=None, executor=None):
     import hashlib
 
     from paper_1503_08294_b200 import FIND_AUTO, Network
-    from paper_1503_08294_b200.multi import resolve_and_update, step
+    from paper_1503_08294_b200.multi import RunState, resolve_and_update, step
     from paper_1503_08294_b200.params import EngineParams, batch_size
 
     case = CASES[name]
@@ -95,6 +102,7 @@ def run_device_trace(name, find_mode=None, executor=None):
     for k in range(2):
         net.add_unit(seeds[k], params.theta0)
     per_batch = []
+    state = RunState()  # one RunState for the whole run (multi.py:152)
     signals = discarded = iterations = 0
     units, converged, extra = 2, False, dict(events=0, windows=0, max_degree=0)
     while signals < params.max_signals:
@@ -111,7 +119,7 @@ def run_device_trace(name, find_mode=None, executor=None):
             extra["max_degree"] = max(extra["max_degree"], int(st.max_degree))
         else:
             winners = executor(net.snapshot(), batch)
-            o = resolve_and_update(net, params, batch, winners)
+            o = resolve_and_update(net, params, batch, winners, state)
             out = (o.processed, o.discarded, o.inserted_units)
             c = net.counts()
             units = c["units"]

@@ -77,6 +77,15 @@ CASES = {
     # paper batch rule (floor 64, cap 8192) on the torus cloud, prefix only
     "paper_rule": dict(source=("cloud", "torus100k"), seed=21,
                        params=dict(theta0=0.15, max_signals=200_000)),
+    # large network (V > 4096): the engine's AUTO find crosses every regime
+    # (screened small find, n <= 6144 FP64 small find, filter / grid) under
+    # the paper batch rule (m up to 8192); V ~ 9.9k after 1.5 M signals
+    "v8k": dict(source=("cloud", "torus100k"), seed=7,
+                params=dict(theta0=0.05, batch_cap=8192, max_signals=1_500_000)),
+    # the same cloud with a fixed m = 8192 (the asynchronous device-sampled path)
+    "v8k_fixed": dict(source=("cloud", "torus100k"), seed=7,
+                      params=dict(theta0=0.05, batch_floor=8192, batch_cap=8192,
+                                  max_signals=1_228_800)),
 }
 
 
@@ -172,7 +181,8 @@ def make_kernel_cases(path):
 def main(only=None):
     sph, tor = clouds()
     cache = {"sphere10k": sph, "torus100k": tor, "hemisphere": hemisphere_cloud()}
-    make_kernel_cases(os.path.join(HERE, "kernel_cases.npz"))
+    if not only or "kernel_cases" in only:
+        make_kernel_cases(os.path.join(HERE, "kernel_cases.npz"))
     for name, case in CASES.items():
         if only and name not in only:
             continue

@@ -72,6 +72,80 @@ def test_off_parse_errors_match_reference(tmp_path, text):
     assert np.array_equal(got.vertices, want.vertices) and np.array_equal(got.faces, want.faces)
 
 
+@pytest.mark.parametrize("text", [
+    "", "0 0 0\n", "1 2\n", "1 2 3 4\n", "1 x 3\n", "# only a comment\n",
+    "1 2 3 # trailing\n\n4 5 6\n", "1e400 0 0\n", "nan inf -inf\n", "0 0 0\n1 2 three\n",
+])
+def test_xyz_parse_matches_reference(tmp_path, text):
+    from paper_1503_08294_b200 import ParseError, load_xyz
+
+    rs = _reference()
+    p = tmp_path / "c.xyz"
+    p.write_text(text)
+    try:
+        want = rs.load_xyz(p)
+    except rs.ParseError as e:
+        with pytest.raises(ParseError) as got:
+            load_xyz(p)
+        assert str(got.value) == str(e)
+        return
+    got = load_xyz(p)
+    assert got.shape == want.shape and np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_stats_csv_byte_identical_to_reference(tmp_path):
+    """write_stats_csv (metrics.py:130-136): same header, field formatting
+    (repr floats, lowercase booleans) and line endings as the reference."""
+    from paper_1503_08294_b200 import RunStats, write_stats_csv
+
+    _reference()
+    import growsurf.metrics as rm
+
+    rows = [
+        dict(variant="multi-b200", dataset="double-torus-1M", seed=7, iterations=6468,
+             signals=26_492_928, discarded=15_654_514, units=1958, connections=5880,
+             total_s=0.5307, sample_s=0.0, find_s=0.0873, update_s=0.4431, converged=True),
+        dict(variant='we"ird,name', dataset="a\nb", seed=0, iterations=0, signals=0,
+             discarded=0, units=2, connections=0, total_s=1e-300, sample_s=float("inf"),
+             find_s=0.1 + 0.2, update_s=-0.0, converged=False),
+    ]
+    write_stats_csv(tmp_path / "a.csv", [RunStats(**r) for r in rows])
+    rm.write_stats_csv(tmp_path / "b.csv", [rm.RunStats(**r) for r in rows])
+    assert (tmp_path / "a.csv").read_bytes() == (tmp_path / "b.csv").read_bytes()
+
+
+def test_run_state_fields_match_reference():
+    """RunState has the reference's fields and fresh values (engine.py:101-119)."""
+    from paper_1503_08294_b200.multi import RunState
+
+    _reference()
+    from growsurf.engine import RunState as RefRunState
+
+    a, b = RunState(), RefRunState()
+    assert set(a.__slots__) == set(b.__slots__)
+    assert (a.tick, a.next_sweep, dict(a.patience), a.last_active) == (
+        b.tick, b.next_sweep, b.patience, b.last_active)
+    assert a.patience[12345] == 0 and 12345 not in a.patience
+
+
+def test_executor_signatures_match_reference():
+    """sequential_executor(backend=None, tile=None) and friends keep the
+    reference's parameter names and order (multi.py:81-96, parallel.py:91-114)."""
+    import inspect
+
+    import paper_1503_08294_b200 as P
+
+    _reference()
+    import growsurf as R
+
+    for name in ("sequential_executor", "parallel_executor", "batch_find_winners",
+                 "parallel_batch_find_winners", "timed_find", "resolve_and_update",
+                 "update_single", "find_winners_exhaustive", "run", "run_multi"):
+        want = list(inspect.signature(getattr(R, name)).parameters)
+        got = list(inspect.signature(getattr(P, name)).parameters)
+        assert got[:len(want)] == want, (name, got, want)
+
+
 def test_exec_config_validation():
     from paper_1503_08294_b200 import ExecConfig
 

@@ -40,6 +40,24 @@ def test_device_run_matches_reference_golden(name):
     net.audit()
 
 
+@pytest.mark.parametrize("name", ["v8k", "v8k_fixed"])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])  # exact, filter, AUTO, screened small, grid
+def test_large_network_find_modes_match_reference(name, mode):
+    """V grows past 4096 (to ~9.9k): the engine's find leaves the screened
+    small kernel (n <= 4096) for the FP64 small kernel (n <= 6144), the
+    filter or the grid, with row->slot indirection and dead rows in the
+    snapshot; every mode must still reproduce the reference's run."""
+    gold = load_golden(name)
+    if not same_numpy(gold):
+        pytest.skip("golden made with another numpy")
+    net, stats, per_batch, digest = run_device_trace(name, find_mode=mode)
+    assert digest == str(gold["signal_sha256"])
+    assert int(gold["stat_units"]) > 4096 and stats["units"] > 4096
+    assert np.array_equal(per_batch, gold["per_batch"])
+    assert_state_equal(net.export(), gold)
+    net.audit()
+
+
 @pytest.mark.parametrize("mode", [0, 1, 3, 4])  # exact, filter, screened small, grid
 def test_find_modes_identical_runs(mode):
     gold = load_golden("stress")
@@ -76,8 +94,10 @@ def test_random_winner_streams_match_oracle():
     """resolve_and_update with adversarial winner lists (many collisions,
     stale seconds, repeated winners) against the oracle's sequential loop."""
     from paper_1503_08294_b200 import EngineParams, Network, WinnerResult, resolve_and_update
+    from paper_1503_08294_b200.multi import RunState
 
     rng = np.random.default_rng(5)
+    state = RunState()  # the oracle keeps one run state across the calls
     params = EngineParams(theta0=0.3, max_age=6, ring_patience=2, stale_factor=1)
     net = Network(params)
     onet = O.OracleNet(params)
@@ -85,6 +105,10 @@ def test_random_winner_streams_match_oracle():
     for p in pts:
         net.add_unit(p, 0.3)
         onet.add_unit(p, 0.3)
+    for k in range(40):  # connected start: isolated units would all be pruned at once
+        for j in (1, 2):
+            net.connect_or_reset(k, (k + j) % 40)
+            onet.connect_or_reset(k, (k + j) % 40)
     for it in range(60):
         ids = np.array(net.unit_ids())
         m = int(rng.integers(1, 300))
@@ -95,7 +119,7 @@ def test_random_winner_streams_match_oracle():
         batch = rng.random((m, 3))
         out = resolve_and_update(net, params, batch,
                                  [WinnerResult(int(x), int(y), float(z), 0.0)
-                                  for x, y, z in zip(b, s, d)])
+                                  for x, y, z in zip(b, s, d)], state)
         want = onet.resolve_and_update(batch, b, s, d)
         assert (out.processed, out.discarded, out.inserted_units) == tuple(int(v) for v in want)
         assert_state_equal(net.export(), onet.export())
@@ -252,7 +276,7 @@ def test_cfg3_headline_run_matches_reference():
     assert manifold_check(mesh) == "closed" and genus(mesh) == 2
 
 
-@pytest.mark.parametrize("name", ["paper_rule", "boundary", "cfg1"])
+@pytest.mark.parametrize("name", ["paper_rule", "boundary", "cfg1", "v8k", "v8k_fixed"])
 def test_run_multi_device_sampling_matches_golden(name):
     """run_multi on a CloudSource draws its batches on the device (variable m
     under the paper's batch rule: synchronous; fixed m: the asynchronous
