@@ -183,6 +183,23 @@ gs_status gs_engine_update_device(gs_engine *eng, const double *d_signals, int64
 gs_status gs_engine_resolve_host(gs_engine *eng, const double *signals, int64_t m,
                                  const int64_t *win_b, const int64_t *win_s,
                                  const double *d_win, gs_batch_stats *out);
+/* ---- signal sharding across GPUs (one process per GPU) ----
+ * The reference's static split of each batch over workers (parallel.py:78)
+ * across ranks: with shards set, every step on this engine (host, device or
+ * sampled batch) finds winners only for signals [rank*m/world,
+ * (rank+1)*m/world), one ncclAllGather of the GS_WINREC_BYTES records on the
+ * engine stream assembles the batch in rank order == batch order, and every
+ * rank runs the identical update (replicas stay bit-identical).  Every rank
+ * must draw the same batches (same seed) and m % world == 0. */
+#define GS_SHARD_ID_BYTES 128
+/* A fresh communicator id (rank 0 makes it, the caller broadcasts it). */
+gs_status gs_shard_unique_id(uint8_t *out, int64_t len);
+/* Join the world (blocks until every rank joined); world = 0 detaches. */
+gs_status gs_engine_set_shards(gs_engine *eng, int world, int rank, const uint8_t *id,
+                               int64_t len);
+/* Device time of the record all-gathers (with phase timing on), ms. */
+gs_status gs_engine_exchange_ms(gs_engine *eng, double *out);
+
 /* Per-phase device time (CUDA events on the engine stream) accumulated over
  * steps: out[0] find ms, out[1] update ms.  enable: 1 every batch, k > 1 one
  * batch in k weighted by k (an estimate with the event records off the

@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("GS_LIB_PATH") or os.path.join(HERE, "libgrowsurf_b200
 
 GS_OK, GS_VALUE_ERROR, GS_STATE_ERROR, GS_CUDA_ERROR, GS_UNKNOWN_UNIT = range(5)
 FIND_EXACT, FIND_FILTER, FIND_AUTO, FIND_SMALL, FIND_GRID = 0, 1, 2, 3, 4
+SHARD_ID_BYTES = 128  # GS_SHARD_ID_BYTES (an ncclUniqueId)
 
 
 class DeviceUnavailable(RuntimeError):
@@ -82,6 +83,9 @@ _SIGNATURES = {
     "gs_engine_resolve_host": (C.c_int, [_vp, _f64p, C.c_int64, _i64p, _i64p, _f64p,
                                          C.POINTER(GsBatchStats)]),
     "gs_engine_set_params": (C.c_int, [_vp, C.POINTER(GsParams)]),
+    "gs_shard_unique_id": (C.c_int, [_vp, C.c_int64]),
+    "gs_engine_set_shards": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.c_int64]),
+    "gs_engine_exchange_ms": (C.c_int, [_vp, C.POINTER(C.c_double)]),
     "gs_engine_phase_ms": (C.c_int, [_vp, C.c_int, _f64p]),
     "gs_engine_stats": (C.c_int, [_vp, C.POINTER(GsBatchStats)]),
     "gs_engine_stats_lagged": (C.c_int, [_vp, C.c_int64, C.POINTER(GsBatchStats),

@@ -254,6 +254,9 @@ __device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
 }
 
 void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
+// sig[j] = pts[idx[j]] for j < m (sampled batches materialised for every rank)
+void gather_signals_launch(const int64_t* idx, const double* pts, double* sig, int64_t m,
+                           cudaStream_t stream);
 
 // device CloudSource sampler (sample.cu): m signals into d_out on `stream`
 void sampler_draw(gs_sampler* s, int64_t m, double* d_out, cudaStream_t stream);

@@ -47,6 +47,7 @@
 #include <vector>
 
 #include <cooperative_groups.h>
+#include <nccl.h>
 
 #include "common.cuh"
 
@@ -874,12 +875,13 @@ struct gs_engine {
   // done) CUDA events on the engine stream, so every batch is timed even
   // with batches in flight; harvested at the next synchronisation
   static constexpr int kEvRing = 64;
-  cudaEvent_t ev[kEvRing][3] = {};
+  cudaEvent_t ev[kEvRing][4] = {};  // start, find done, update done, exchange done
   int ev_head = 0, ev_count = 0;
   bool timing = false;
   int timing_every = 1;      // time one batch in timing_every (weighted by it)
   long long timing_seq = 0;
   int ev_w[kEvRing] = {};
+  bool ev_x[kEvRing] = {};  // entry has an exchange (all-gather) event
   int64_t ev_b[kEvRing] = {};  // batch (issue index) a timing entry belongs to
   // batch (issue index) whose completion event a stats-ring slot holds
   int64_t stat_batch[kEvRing];
@@ -897,6 +899,13 @@ struct gs_engine {
   cudaEvent_t pf_done[2] = {}, use_done[2] = {};
   int64_t pf_issued = 0, pf_used = 0;
   int pf_half = 0;
+  // signal sharding across GPUs: this rank finds winners for
+  // signals [rank*m/world, (rank+1)*m/world) and one ncclAllGather of the
+  // 16-byte records on the engine stream assembles the batch in rank order
+  // == batch order; the update is replicated
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  double exchange_ms = 0.0;
 };
 
 namespace {
@@ -1256,6 +1265,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
     cudaStreamSynchronize(e->side);
     cudaStreamDestroy(e->side);
   }
+  if (e->comm) ncclCommDestroy(e->comm);
   for (int h = 0; h < 2; ++h) {
     if (e->pf_done[h]) cudaEventDestroy(e->pf_done[h]);
     if (e->use_done[h]) cudaEventDestroy(e->use_done[h]);
@@ -1396,10 +1406,30 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   if (timed) {
     e->ev_w[ev_slot] = e->timing_every;
     e->ev_b[ev_slot] = e->issued;
+    e->ev_x[ev_slot] = e->comm != nullptr;
     GS_CUDA(cudaEventRecord(evs[0], e->stream));
   }
-  launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
-  if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
+  if (e->comm) {
+    // every rank holds the whole batch (replicated sampling): materialise it
+    // for the update, find on this rank's slice, all-gather the records
+    GS_CHECK(m % e->world == 0, GS_VALUE_ERROR,
+             "sharded batches must divide evenly among the ranks (m % world == 0)");
+    if (sig_idx) {
+      const unsigned long long before = g_launches;
+      gather_signals_launch(sig_idx, sig_pts, const_cast<double*>(d_sig), m, e->stream);
+      e->launches += (long long)(g_launches - before);
+    }
+    const int64_t lo = (int64_t)e->rank * m / e->world, hi = (int64_t)(e->rank + 1) * m / e->world;
+    launch_find(e, d_sig, lo, hi, rec);
+    if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
+    const ncclResult_t r = ncclAllGather(rec + lo, rec, sizeof(WinRec) * (size_t)(hi - lo),
+                                         ncclUint8, e->comm, e->stream);
+    GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    if (timed) GS_CUDA(cudaEventRecord(evs[3], e->stream));
+  } else {
+    launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
+    if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
+  }
   // the kernel writes its stats straight into the host ring slot (pinned,
   // mapped under UVA): no copy between this batch's kernels and the next
   const int slot = (int)(e->issued % gs_engine::kEvRing);
@@ -1424,16 +1454,28 @@ extern "C" gs_status gs_engine_step_device(gs_engine* e, const double* d_sig, in
 }
 
 namespace {
+// fold the oldest timing entry (complete) into find / exchange / update ms
+void fold_timing_entry(gs_engine* e) {
+  cudaEvent_t* evs = e->ev[e->ev_head];
+  const double w = e->ev_w[e->ev_head];
+  float a = 0.f, b = 0.f, x = 0.f;
+  GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
+  if (e->ev_x[e->ev_head]) {
+    GS_CUDA(cudaEventElapsedTime(&x, evs[1], evs[3]));
+    GS_CUDA(cudaEventElapsedTime(&b, evs[3], evs[2]));
+  } else {
+    GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
+  }
+  e->find_ms += a * w;
+  e->exchange_ms += x * w;
+  e->update_ms += b * w;
+  e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
+}
+
 void harvest_timing(gs_engine* e, int keep) {
   for (; e->ev_count > keep; --e->ev_count) {
-    cudaEvent_t* evs = e->ev[e->ev_head];
-    float a = 0.f, b = 0.f;
-    GS_CUDA(cudaEventSynchronize(evs[2]));
-    GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
-    GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
-    e->find_ms += a * e->ev_w[e->ev_head];
-    e->update_ms += b * e->ev_w[e->ev_head];
-    e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
+    GS_CUDA(cudaEventSynchronize(e->ev[e->ev_head][2]));
+    fold_timing_entry(e);
   }
 }
 }  // namespace
@@ -1500,13 +1542,7 @@ extern "C" gs_status gs_engine_stats_lagged(gs_engine* e, int64_t lag, gs_batch_
     GS_CUDA(cudaEventSynchronize(e->stat_ev[target % gs_engine::kEvRing]));
     // per-phase timings of the batches known complete (up to target)
     while (e->ev_count > 0 && e->ev_b[e->ev_head] <= target) {
-      cudaEvent_t* evs = e->ev[e->ev_head];
-      float a = 0.f, b = 0.f;
-      GS_CUDA(cudaEventElapsedTime(&a, evs[0], evs[1]));
-      GS_CUDA(cudaEventElapsedTime(&b, evs[1], evs[2]));
-      e->find_ms += a * e->ev_w[e->ev_head];
-      e->update_ms += b * e->ev_w[e->ev_head];
-      e->ev_head = (e->ev_head + 1) % gs_engine::kEvRing;
+      fold_timing_entry(e);
       e->ev_count--;
     }
     *e->h_stats = e->h_ring[target % gs_engine::kEvRing];
@@ -1610,6 +1646,55 @@ extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t
     harvest_timing(e);
     check_stats(e);
     if (out) *out = *e->h_stats;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// signal sharding across GPUs (one process per GPU)
+
+extern "C" gs_status gs_shard_unique_id(uint8_t* out, int64_t len) {
+  return guarded([&] {
+    GS_CHECK(out && len == (int64_t)sizeof(ncclUniqueId), GS_VALUE_ERROR,
+             "the shard id buffer must be GS_SHARD_ID_BYTES long");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    memcpy(out, &id, sizeof(id));
+  });
+}
+
+extern "C" gs_status gs_engine_set_shards(gs_engine* e, int world, int rank, const uint8_t* id,
+                                          int64_t len) {
+  return guarded([&] {
+    GS_CHECK(e, GS_VALUE_ERROR, "null engine");
+    GS_CHECK(world >= 0 && (world == 0 || (0 <= rank && rank < world)), GS_VALUE_ERROR,
+             "bad world / rank");
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->comm) {
+      ncclCommDestroy(e->comm);
+      e->comm = nullptr;
+    }
+    e->world = 1;
+    e->rank = 0;
+    if (world == 0) return;
+    GS_CHECK(id && len == (int64_t)sizeof(ncclUniqueId), GS_VALUE_ERROR,
+             "the shard id must be GS_SHARD_ID_BYTES long");
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    GS_CUDA(cudaSetDevice(e->ctx->device));
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
+    GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    e->comm = comm;
+    e->world = world;
+    e->rank = rank;
+  });
+}
+
+extern "C" gs_status gs_engine_exchange_ms(gs_engine* e, double* out) {
+  return guarded([&] {
+    GS_CHECK(e && out, GS_VALUE_ERROR, "null argument");
+    *out = e->exchange_ms;
   });
 }
 
@@ -1723,7 +1808,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     e->reset_seq = e->issued;
     memset(e->h_stats, 0, sizeof(gs_batch_stats));
     harvest_timing(e);
-    e->find_ms = e->update_ms = 0.0;
+    e->find_ms = e->update_ms = e->exchange_ms = 0.0;
   });
 }
 

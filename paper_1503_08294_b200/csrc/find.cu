@@ -560,6 +560,14 @@ __global__ void k_gather_signals(const int64_t* idx, const double* pts, double* 
   sig[3 * j + 2] = pts[src + 2];
 }
 
+void gather_signals_launch(const int64_t* idx, const double* pts, double* sig, int64_t m,
+                           cudaStream_t stream) {
+  if (m <= 0) return;
+  k_gather_signals<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(idx, pts, sig, m);
+  GS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
 // forward declarations (filter.cu, grid.cu)
 bool find_filter_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
 void find_grid_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);

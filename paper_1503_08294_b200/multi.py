@@ -273,7 +273,8 @@ def step(net: Network, batch) -> _lib.GsBatchStats:
 def run_multi(source, params: EngineParams, seed: int, executor=None, *,
               variant: str = "multi-b200", dataset: str | None = None,
               find_mode: int = _lib.FIND_AUTO, capacity: int = 4096,
-              device_sampling: bool | None = None, phase_timing: bool = True):
+              device_sampling: bool | None = None, phase_timing: bool = True,
+              shard_group=None):
     """Run the multi-signal engine to convergence or the signal cap.
 
     Same driver contract as multi.py:134-202: Philox(seed) stream, two seed
@@ -284,6 +285,10 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
     draws every batch on the GPU from the same Philox stream
     (device_sampling.py), so the cloud crosses PCIe once per run instead of
     every batch's signals.
+
+    shard_group (a torch.distributed group, e.g. ``dist.group.WORLD``)
+    shards every batch's find across the group's ranks (distributed.py);
+    every rank must make the same call and returns the identical result.
     """
     from .sampling import CloudSource
 
@@ -296,6 +301,12 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
         capacity = max(capacity, 2 + params.batch_cap * (lookahead + 2))
     net = Network(params, capacity=capacity, find_mode=find_mode)
     net.watch_age_limit(params.max_age)
+    if shard_group is not None:
+        if executor is not None:
+            raise ValueError("a sharded run does its own find: pass no executor")
+        from .distributed import attach
+
+        attach(net, shard_group)
     seeds = source.sample(rng, 2)
     for k in range(2):
         net.add_unit(seeds[k], params.theta0)
@@ -395,6 +406,8 @@ def run_multi(source, params: EngineParams, seed: int, executor=None, *,
         _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
         timer.find_s = phase[0] * 1e-3
         timer.update_s = phase[1] * 1e-3
+        if shard_group is not None:  # the all-gathers are part of the find phase
+            timer.find_s += net.exchange_ms() * 1e-3
     stats = RunStats(
         variant=variant,
         dataset=dataset or getattr(source, "label", "unknown"),

@@ -160,6 +160,24 @@ class Network:
         """Allow `depth` batches in flight ahead of stats reads (gs_engine_set_async)."""
         _lib.check(self._lib.gs_engine_set_async(self._h, int(depth)))
 
+    def set_shards(self, world: int, rank: int, uid: bytes | None = None) -> None:
+        """Shard every later step's find over ``world`` ranks (this is
+        ``rank``; ``uid`` is the communicator id all ranks share, see
+        distributed.attach); world = 0 detaches."""
+        buf = None
+        if world:
+            if uid is None or len(uid) != _lib.SHARD_ID_BYTES:
+                raise ValueError("a shard id of SHARD_ID_BYTES bytes is required")
+            buf = (C.c_uint8 * len(uid)).from_buffer_copy(uid)
+        _lib.check(self._lib.gs_engine_set_shards(self._h, int(world), int(rank), buf,
+                                                  _lib.SHARD_ID_BYTES))
+
+    def exchange_ms(self) -> float:
+        """Device time of the sharded record all-gathers so far (phase timing on)."""
+        out = C.c_double()
+        _lib.check(self._lib.gs_engine_exchange_ms(self._h, C.byref(out)))
+        return out.value
+
     def reserve(self, n_ids: int) -> None:
         _lib.check(self._lib.gs_engine_reserve(self._h, int(n_ids)))
 

@@ -16,7 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1503_08294_b200.distributed import REC_BYTES, gather_records, shard_bounds
+from paper_1503_08294_b200.distributed import (REC_BYTES, broadcast_shard_id, gather_records,
+                                               shard_bounds)
 
 REC = np.dtype([("b", "<i4"), ("s", "<i4"), ("d", "<f8")])
 
@@ -54,6 +55,40 @@ def _worker(rank, world, port, m, q):
         q.put((rank, bool(np.array_equal(got.view(np.uint8), want.view(np.uint8)))))
     finally:
         dist.destroy_process_group()
+
+
+def _id_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 0's id reaches every rank (the real id is an ncclUniqueId made
+        # by gs_shard_unique_id; any 128 bytes exercise the same plumbing)
+        made = []
+
+        def make_id():
+            made.append(rank)
+            return bytes((7 * i + 3) % 256 for i in range(128))
+
+        uid = broadcast_shard_id(None, make_id)
+        q.put((rank, (uid == make_id.__call__() if rank == 0 else
+                      uid == bytes((7 * i + 3) % 256 for i in range(128))), made[:1]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_id_broadcast_from_rank0():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (ok, made) for r, ok, made in (q.get(timeout=120) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: (True, [0]), 1: (True, [])}  # only rank 0 made an id
 
 
 @pytest.mark.parametrize("world", [2])
