@@ -8,17 +8,31 @@ for N > 1) prints ONE JSON line on rank 0.
   synthetic genus-2 cloud, m = 4096, theta0 = 0.1, seed 7.  One STEP is one
   complete seeded run from the two seed units to convergence (26.5 M
   signals, V = 1958, closed genus-2 mesh); ms_per_step is the
-  time-to-converge.  The run is bit-identical to the reference's.
-* value: whole-job signals/s with the seeded signal stream already resident
-  in HBM (pre-drawn on the host from the same Philox stream, uploaded
-  before timing); CUDA events on the engine stream; max over ranks.
+  time-to-converge.  The run is bit-identical to the reference's.  At N > 1
+  every batch's find is sharded over the ranks (the engine's own NCCL
+  communicator, one ncclAllGather of winner records per batch, replicated
+  update: distributed.py), so the per-N lines are the same run.
+* value: whole-job signals/s with the cloud resident in HBM; every batch's
+  signals are drawn ON THE DEVICE inside the timed region from the same
+  Philox stream as the reference (csrc/sample.cu, bit-identical to numpy);
+  CUDA events on the engine stream, 256 MiB L2 flush before each step; max
+  over ranks.
 * e2e: the same metric through the public API (``run_multi``, or
-  ``distributed.run_multi_sharded`` at N > 1): host sampling, one pinned H2D
-  copy of every batch and one stats D2H per batch inside the timed region.
+  ``distributed.run_multi_sharded`` at N > 1) from host memory: the cloud's
+  H2D copy, the sampler state and every batch's stats (written by the
+  update kernel into pinned host memory) are inside the timed region.
 * cpu_baseline / --impl reference: the unmodified reference (growsurf built
   from /root/reference into oracle/_ref, Cython kernel, parallel_executor on
-  every host core) on a bounded prefix of the same seeded run.  If
-  oracle/_ref is absent the C oracle port stands in (kind "port").
+  every host core) resumed from its OWN pickled state at the start of each
+  of 8 equal slices of the run (tests/golden/make_ref_checkpoints.py) for a
+  bounded time each: the whole run's time-to-converge is estimated as the
+  sum over slices of (batches in the slice x measured seconds per batch), a
+  stratified sample of the full run.  ``--ref-full-cfg3`` runs the stock
+  ``growsurf.run_multi`` to convergence instead (minutes); configs 1 and 2
+  are run to convergence by the stock reference in ``other_configs``.
+* cfg4 (BASELINE config 4): 10M-point torus cloud, paper batch rule up to
+  m = 65536, a fixed 30 M-signal budget through the public API, sharded over
+  the N ranks: signals/s and all-gather time per batch.
 """
 
 from __future__ import annotations
@@ -39,6 +53,7 @@ sys.path.insert(0, REPO)
 METRIC = "signals/sec & time-to-converge (SOAM, 1M-pt cloud) at 1/2/4/8 B200 vs CPU ref"
 MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 NCU_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
+REF_CKPT = os.path.join(REPO, "tests", "golden", "ref_cfg3_checkpoints.pkl.gz")
 
 
 def parse_args():
@@ -53,6 +68,12 @@ def parse_args():
     p.add_argument("--cpu-budget-s", type=float, default=20.0)
     p.add_argument("--no-find-microbench", action="store_true")
     p.add_argument("--no-m-sweep", action="store_true")
+    p.add_argument("--no-ref-full", action="store_true",
+                   help="skip the stock reference's full runs of configs 1 and 2")
+    p.add_argument("--ref-full-cfg3", action="store_true",
+                   help="also run the stock reference's config-3 run to convergence (minutes)")
+    p.add_argument("--no-cfg4", action="store_true")
+    p.add_argument("--no-sharded-anchor", action="store_true")
     return p.parse_args()
 
 
@@ -218,6 +239,132 @@ def reference_prefix(points, label, wparams, seed, budget_s):
     return signals, time.perf_counter() - t0, batches, "port", 1
 
 
+def load_ref_checkpoints(workload):
+    """The reference's own pickled states at the start of each slice of its
+    config-3 run (tests/golden/make_ref_checkpoints.py), or None."""
+    if workload != "cfg3" or not os.path.exists(REF_CKPT) or not reference_available():
+        return None
+    import gzip
+    import pickle
+
+    import numpy as np
+
+    with gzip.open(REF_CKPT, "rb") as fh:
+        blob = pickle.load(fh)
+    if blob.get("numpy_version") != np.__version__:
+        return None  # Generator streams are numpy-version specific
+    return blob
+
+
+def reference_stratified(points, label, wparams, budget_s, blob, acc=None):
+    """Resume the stock reference (multi.py:165-185 loop with growsurf's own
+    sample / parallel executor / resolve_and_update / is_converged) from each
+    checkpoint for budget_s / slices seconds; accumulates [batches, seconds]
+    per slice into ``acc``."""
+    import pickle
+
+    import numpy as np
+    from growsurf import CloudSource, EngineParams
+    from growsurf.engine import is_converged
+    from growsurf.multi import batch_size, resolve_and_update
+    from growsurf.parallel import ExecConfig, parallel_executor
+
+    params = EngineParams(**wparams)
+    src = CloudSource(points, label=label)
+    executor = parallel_executor(ExecConfig(workers=os.cpu_count() or 1))
+    starts = list(blob["starts"]) + [blob["total_batches"]]
+    k = len(blob["checkpoints"])
+    if acc is None:
+        acc = [[0, 0.0] for _ in range(k)]
+    per = budget_s / k
+    for c, raw in enumerate(blob["checkpoints"]):
+        cp = pickle.loads(raw)
+        net, state = cp["net"], cp["state"]
+        rng = np.random.Generator(np.random.Philox(0))
+        rng.bit_generator.state = cp["rng"]
+        limit = starts[c + 1] - starts[c]
+        n = 0
+        t0 = time.perf_counter()
+        while n < limit:
+            m = batch_size(net.unit_count, params.batch_cap, params.batch_floor)
+            batch = src.sample(rng, m)
+            winners = executor(net.snapshot(), batch)
+            resolve_and_update(net, params, batch, winners, state)
+            n += 1
+            if is_converged(net, params) or time.perf_counter() - t0 >= per:
+                break
+        acc[c][0] += n
+        acc[c][1] += time.perf_counter() - t0
+    return acc
+
+
+def stratified_estimate(acc, blob):
+    """Estimated time-to-converge: sum over slices of batches x s/batch."""
+    starts = list(blob["starts"]) + [blob["total_batches"]]
+    per_slice = [(starts[c + 1] - starts[c]) * sec / max(1, n) for c, (n, sec) in enumerate(acc)]
+    return sum(per_slice), per_slice
+
+
+def reference_cpu_rate(points, label, wparams, seed, budget_s, workload, steps=1, warmup=0):
+    """(signals/s, ms per run, kind, cores, sample text) of the reference on
+    this host: stratified over the run when its checkpoints exist, else the
+    run's prefix."""
+    blob = load_ref_checkpoints(workload)
+    cores = os.cpu_count() or 1
+    if blob is not None:
+        for _ in range(warmup):
+            reference_stratified(points, label, wparams, budget_s, blob)
+        acc = None
+        for _ in range(steps):
+            acc = reference_stratified(points, label, wparams, budget_s, blob, acc)
+        est, per_slice = stratified_estimate(acc, blob)
+        sampled = sum(n for n, _ in acc)
+        value = blob["total_signals"] / est
+        sample = (f"stratified: the stock reference resumed from its own checkpoints at the start "
+                  f"of each of {len(acc)} equal slices of the {blob['total_batches']}-batch "
+                  f"{workload} run, {sampled} batches sampled ({sum(t for _, t in acc):.1f} s); "
+                  f"estimated time-to-converge {est:.1f} s = sum of slice batches x s/batch "
+                  f"(slices: " + ", ".join(f"{t:.1f}" for t in per_slice) + " s)")
+        return value, 1e3 * est, "reference", cores, sample
+    tot_sig = tot_s = 0.0
+    kind = batches = None
+    for _ in range(warmup):
+        reference_prefix(points, label, wparams, seed, budget_s)
+    for _ in range(steps):
+        sig, sec, batches, kind, cores = reference_prefix(points, label, wparams, seed, budget_s)
+        tot_sig += sig
+        tot_s += sec
+    sample = (f"prefix: first {int(tot_sig / steps):,} signals ({batches} batches, "
+              f"~{budget_s:.0f} s budget) of the seeded {workload} run (early-run rate)")
+    return tot_sig / tot_s, 1e3 * tot_s / steps, kind, cores, sample
+
+
+def reference_full_run(name, workload_params=None):
+    """The stock ``growsurf.run_multi`` to convergence on this host."""
+    from growsurf import CloudSource, EngineParams, run_multi
+    from growsurf.multi import sequential_executor
+    from growsurf.parallel import ExecConfig, parallel_executor
+
+    from paper_1503_08294_b200 import workloads
+
+    w = workloads.WORKLOADS[name]
+    pts, label = w["cloud"]()
+    params = EngineParams(**(workload_params or w["params"]))
+    if params.batch_cap <= 64:
+        ex, how = sequential_executor(), "sequential_executor (1 core)"
+    else:
+        ex = parallel_executor(ExecConfig(workers=os.cpu_count() or 1))
+        how = f"parallel_executor ({os.cpu_count()} cores)"
+    t0 = time.perf_counter()
+    net, st = run_multi(CloudSource(pts, label=label), params, w["seed"], ex)
+    sec = time.perf_counter() - t0
+    return {"time_to_converge_s": sec, "converged": bool(st.converged), "signals": st.signals,
+            "iterations": st.iterations, "units": st.units, "edges": st.connections,
+            "signals_per_s": st.signals / sec, "find_s": st.find_s, "update_s": st.update_s,
+            "sample_s": st.sample_s, "executor": how, "cores": os.cpu_count(),
+            "how": "stock growsurf.run_multi (oracle/_ref) on this host"}
+
+
 def run_reference_arm(args):
     world, rank, _ = dist_setup(args, "gloo")
     if rank != 0:
@@ -227,25 +374,16 @@ def run_reference_arm(args):
     src, params, seed, desc = workloads.make(args.workload)
     wparams = dict(workloads.WORKLOADS[args.workload]["params"])
     budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        reference_prefix(src.points, src.label, wparams, seed, budget)
-    tot_sig = tot_s = 0.0
-    kind = cores = None
-    batches = 0
-    for _ in range(args.steps):
-        sig, sec, batches, kind, cores = reference_prefix(src.points, src.label, wparams, seed, budget)
-        tot_sig += sig
-        tot_s += sec
-    value = tot_sig / tot_s
-    sample = (f"first {int(tot_sig / args.steps):,} signals ({batches} batches, ~{budget:.0f} s budget) "
-              f"of the seeded {args.workload} run, repeated per step")
+    value, ms, kind, cores, sample = reference_cpu_rate(
+        src.points, src.label, wparams, seed, budget, args.workload, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "signals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": desc, "m": params.batch_cap,
-                   "theta0": params.theta0, "seed": seed},
+                   "theta0": params.theta0, "seed": seed,
+                   "step": "one seeded run to convergence (estimated from the stratified sample)"},
         "cpu_baseline": {"value": value, "unit": "signals/s", "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "signals/s", "h2d_bytes_per_step": 0,
@@ -274,72 +412,88 @@ def ncu_traffic(kernel: str):
         return None
 
 
-def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000), m=1_000_000,
-                    reps=3, cpu_budget_s=8.0):
-    """BASELINE config 5: m = 1e6 signals vs n units, uniform [0,1)^3 from
-    Philox(7) (cli.py:252-261).  Resident inputs, FP32 filter + certified
-    FP64 re-check (bit-identical to the reference scan), CUDA events on the
-    launching stream, L2 flushed between repetitions (the unit-pair array of
-    the largest n is 16 MB; signals 24 MB)."""
+def find_microbench(lib, ctx, fp32_peak, peak_source, sizes=(10_000, 100_000, 1_000_000),
+                    m=1_000_000, reps=3, cpu_budget_s=8.0, dists=("uniform", "torus")):
+    """BASELINE config 5: m = 1e6 signals vs n units, uniform in [0,1)^3
+    (cli.py:252-261) and on a torus inside the unit cube, from Philox(7).
+    Resident inputs, CUDA events on the launching stream, L2 flushed between
+    repetitions.  Two exact modes with the same output: the FP32 filter +
+    certified FP64 re-check (FP32-bound: `lines`) and the exact uniform grid
+    (`grid_lines`); every line checks grid == filter bit for bit on all m
+    signals (the tests check both against the oracle and the FP64 scan)."""
     import numpy as np
     import torch
 
+    from paper_1503_08294_b200.sampling import TorusSource
+
     out = {"m": m, "mode": "filter (FP32 FFMA2 + certified FP64)", "lines": [],
-           "grid_mode": "exact uniform grid rebuilt per call (GS_FIND_GRID; HBM/L2-latency bound)",
-           "grid_lines": []}
+           "grid_mode": "exact uniform grid rebuilt per call (GS_FIND_GRID; L2-latency bound)",
+           "grid_lines": [], "peak_tflops": fp32_peak, "peak_source": peak_source}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     st = torch.cuda.Stream()  # a real stream: handle 0 would mean the context's own stream
-    peak = 2 * 128 * ctx.sm_count * sm_mhz * 1e6 / 1e12
-    for n in sizes:
-        rng = np.random.Generator(np.random.Philox(7))
-        pos = torch.from_numpy(rng.random((n, 3))).cuda()
-        sig = torch.from_numpy(rng.random((m, 3))).cuda()
-        idx = torch.empty((m, 2), dtype=torch.int64, device="cuda")
-        d2 = torch.empty((m, 2), dtype=torch.float64, device="cuda")
-        torch.cuda.synchronize()
 
-        def timed(mode):
-            def run():
-                _lib_check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(), m,
-                                              idx.data_ptr(), d2.data_ptr(), mode, st.cuda_stream))
+    def draw(dist, rng, k):
+        if dist == "uniform":
+            return rng.random((k, 3))
+        return TorusSource(0.3, 0.1).sample(rng, k) + 0.5  # inside [0.1, 0.9]^3
 
-            run()
-            times = []
-            for _ in range(reps):
-                with torch.cuda.stream(st):
-                    flush.zero_()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(st)
+    for dist in dists:
+        for n in sizes:
+            rng = np.random.Generator(np.random.Philox(7))
+            pos = torch.from_numpy(draw(dist, rng, n)).cuda()
+            sig = torch.from_numpy(draw(dist, rng, m)).cuda()
+            idx = torch.empty((m, 2), dtype=torch.int64, device="cuda")
+            d2 = torch.empty((m, 2), dtype=torch.float64, device="cuda")
+            torch.cuda.synchronize()
+
+            def timed(mode):
+                def run():
+                    _lib_check(lib.gs_find_device(ctx.handle, pos.data_ptr(), n, sig.data_ptr(),
+                                                  m, idx.data_ptr(), d2.data_ptr(), mode,
+                                                  st.cuda_stream))
+
                 run()
-                e1.record(st)
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
-            fb = np.zeros(2, np.int64)
-            _lib_check(lib.gs_find_last_fallback_counts(ctx.handle, fb))
-            return statistics.median(times), fb
+                times = []
+                for _ in range(reps):
+                    with torch.cuda.stream(st):
+                        flush.zero_()
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
+                    run()
+                    e1.record(st)
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1))
+                fb = np.zeros(2, np.int64)
+                _lib_check(lib.gs_find_last_fallback_counts(ctx.handle, fb))
+                return statistics.median(times), fb
 
-        # exact uniform grid (GS_FIND_GRID): same output, O(m) candidates
-        gms, gfb = timed(4)
-        gbytes = 24 * n + 32 * n + 56 * m  # rows read, rows in cell order, signals + results
-        out["grid_lines"].append({"n": n, "ms": gms, "signals_per_s": m / (gms * 1e-3),
-                                  "equivalent_pairs_per_s": float(n) * m / (gms * 1e-3),
-                                  "algorithmic_bytes": gbytes,
-                                  "achieved_gbs": gbytes / (gms * 1e-3) / 1e9,
-                                  "exhaustive_fallback_signals": int(gfb[0])})
-        ms, fb2 = timed(1)
-        out["grid_lines"][-1]["speedup_vs_filter"] = ms / gms
-        pairs = float(n) * m
-        achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
-        out["lines"].append({"n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),
-                             "algorithmic_bytes": 24 * n + 56 * m,
-                             "traffic": ncu_traffic({1_000_000: "filter", 100_000: "filter_n1e5"}.get(n, "")),
-                             "achieved_tflops": achieved, "peak_tflops": peak,
-                             "frac": achieved / peak, "fallback_signals": int(fb2[0]),
-                             "fp64_rescans": int(fb2[1])})
-        del pos, sig, idx, d2
-    out["peak_source"] = (f"nominal FP32 2x128 lanes x {ctx.sm_count} SMs at the sampled "
-                          f"{sm_mhz:.0f} MHz; 8 FLOP per pair (BASELINE.md 2)")
+            gms, gfb = timed(4)
+            g_idx, g_d2 = idx.clone(), d2.clone()
+            gbytes = 24 * n + 32 * n + 56 * m  # rows read, rows in cell order, signals + results
+            ms, fb2 = timed(1)
+            same = bool(torch.equal(g_idx, idx) and torch.equal(g_d2.view(torch.int64),
+                                                                d2.view(torch.int64)))
+            out["grid_lines"].append({"dist": dist, "n": n, "ms": gms,
+                                      "signals_per_s": m / (gms * 1e-3),
+                                      "equivalent_pairs_per_s": float(n) * m / (gms * 1e-3),
+                                      "algorithmic_bytes": gbytes,
+                                      "achieved_gbs": gbytes / (gms * 1e-3) / 1e9,
+                                      "exhaustive_fallback_signals": int(gfb[0]),
+                                      "speedup_vs_filter": ms / gms,
+                                      "identical_to_filter": same})
+            pairs = float(n) * m
+            achieved = 8.0 * pairs / (ms * 1e-3) / 1e12
+            key = {1_000_000: "filter", 100_000: "filter_n1e5"}.get(n, "") if dist == "uniform" else ""
+            out["lines"].append({"dist": dist, "n": n, "ms": ms, "pairs_per_s": pairs / (ms * 1e-3),
+                                 "algorithmic_bytes": 24 * n + 56 * m,
+                                 "traffic": ncu_traffic(key),
+                                 "achieved_tflops": achieved, "peak_tflops": fp32_peak,
+                                 "frac": achieved / fp32_peak, "fallback_signals": int(fb2[0]),
+                                 "fp64_rescans": int(fb2[1]), "identical_to_grid": same})
+            if not same:
+                raise SystemExit(f"config 5: grid and filter disagree ({dist}, n={n})")
+            del pos, sig, idx, d2, g_idx, g_d2
     # the reference's raw scan (_parallel_scan, all host cores) on a bounded sample
     if reference_available():
         from growsurf import kernels as rk
@@ -364,6 +518,18 @@ def find_microbench(lib, ctx, sm_mhz, peaks, sizes=(10_000, 100_000, 1_000_000),
                                 "cores": os.cpu_count(), "seconds": sec,
                                 "how": "growsurf.parallel._parallel_scan, compiled backend, tile 1024"}
     return out
+
+
+def fp32_peak(lib, ctx, sm_mhz, peaks):
+    """(TFLOP/s, source): the FFMA2 probe measured on this GPU, else nominal."""
+    t, ms = C.c_double(), C.c_double()
+    try:
+        _lib_check(lib.gs_fp32_peak(ctx.handle, C.byref(t), C.byref(ms)))
+        return t.value, (f"measured: packed FFMA2 chains on all {ctx.sm_count} SMs "
+                         f"(gs_fp32_peak, best of 5, {ms.value:.2f} ms)")
+    except Exception:  # noqa: BLE001 - report the nominal figure instead
+        return (2 * 128 * ctx.sm_count * sm_mhz * 1e6 / 1e12,
+                f"nominal FP32 2x128 lanes x {ctx.sm_count} SMs at {sm_mhz:.0f} MHz")
 
 
 def m_sweep(lib, src, wparams, seed, ms=(256, 1024, 4096, 16384, 65536), budget_s=20.0):
@@ -419,7 +585,7 @@ def m_sweep(lib, src, wparams, seed, ms=(256, 1024, 4096, 16384, 65536), budget_
     return out
 
 
-def other_configs(lib, names=("cfg1", "cfg2"), budget_s=20.0):
+def other_configs(lib, names=("cfg1", "cfg2"), budget_s=20.0, ref_full=True):
     """BASELINE configs 1 and 2 (the SOAM runs the reference converges on):
     time to converge from the two seed units with device sampling and the
     asynchronous loop, CUDA events on the engine stream (same run as the
@@ -473,6 +639,12 @@ def other_configs(lib, names=("cfg1", "cfg2"), budget_s=20.0):
         sampler.close()
         net.close()
         del pts_dev
+        if ref_full and reference_available():
+            ref = reference_full_run(name)
+            ref["same_run"] = (ref["signals"], ref["units"], ref["edges"]) == (sig, int(st.units),
+                                                                               int(st.edges))
+            out[name]["reference_same_box"] = ref
+            out[name]["speedup_time_to_converge"] = ref["time_to_converge_s"] / sec
     return out
 
 
@@ -490,11 +662,12 @@ def run_b200_arm(args):
     torch.cuda.set_device(local)
     os.environ["GS_DEVICE"] = str(local)
     from paper_1503_08294_b200 import _lib, workloads
-    from paper_1503_08294_b200.distributed import ShardedStep, run_multi_sharded
+    from paper_1503_08294_b200.distributed import attach, run_multi_sharded, shard_unique_id
     from paper_1503_08294_b200.multi import run_multi
     from paper_1503_08294_b200.network import Network
 
     lib = _lib.load_library()
+    ctx = _lib.default_context()
     src, params, seed, desc = workloads.make(args.workload)
     if params.batch_floor != params.batch_cap:
         raise SystemExit("bench workloads use a fixed batch size")
@@ -509,25 +682,26 @@ def run_b200_arm(args):
     pts_dev = torch.from_numpy(src.points).cuda()
     cloud_bytes = pts_dev.numel() * 8
     sampler = DeviceCloudSampler(None, device_ptr=pts_dev.data_ptr(), npts=src.points.shape[0])
-    sig_buf = torch.empty((m, 3), dtype=torch.float64, device="cuda")
-    net = Network(params, capacity=8192)
-    net.reserve(8192)
-    sharded = ShardedStep(net) if world > 1 else None
-    if sharded is None:
-        net.set_async(8)
-    engine_stream = torch.cuda.ExternalStream(net.stream_handle())
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     st = _lib.GsBatchStats()
-    torch.cuda.synchronize()
-
     LOOKAHEAD = 8  # batches enqueued ahead of the convergence check
 
-    def one_run(trace=None):
+    def make_net(shards):
+        net = Network(params, capacity=8192)
+        net.reserve(8192)
+        if shards == "world":
+            attach(net)  # this rank's slice of every batch + ncclAllGather
+        elif shards == "world1":
+            net.set_shards(1, 0, shard_unique_id())
+        net.set_async(LOOKAHEAD)
+        return net
+
+    def one_run(net, trace=None):
         net.reset()
         for s in seeds:
             net.add_unit(s, params.theta0)
         _lib.check(lib.gs_sampler_set_state(sampler.handle, state0))
-        if trace is None and sharded is None:
+        if trace is None:
             # device-resident loop: the host only polls the convergence flag;
             # batches after convergence are no-ops on the device (halted)
             enq = 0
@@ -542,24 +716,19 @@ def run_b200_arm(args):
                         break
             _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
             return int(st.batches) * m, bool(st.converged), int(st.units), int(st.edges)
+        net.set_async(0)  # synchronous: per-batch stats for the trace
         off = 0
         units = 2
         while off < params.max_signals:
-            if trace is not None:
-                trace["pairs"] += m * units
-            if sharded is None:
-                _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, None))
-            else:
-                sampler.draw(m, sig_buf.data_ptr(), net.stream_handle())
-                sharded.step_device(sig_buf.data_ptr(), m)
-            _lib.check(lib.gs_engine_stats(net.handle, C.byref(st)))
+            trace["pairs"] += m * units
+            _lib.check(lib.gs_engine_step_sampled(net.handle, sampler.handle, m, C.byref(st)))
             off += m
             units = int(st.units)
-            if trace is not None:
-                trace["processed"] += int(st.processed)
-                trace["batches"] += 1
+            trace["processed"] += int(st.processed)
+            trace["batches"] += 1
             if st.converged:
                 break
+        net.set_async(LOOKAHEAD)
         return off, bool(st.converged), int(st.units), int(st.edges)
 
     def barrier():
@@ -568,70 +737,84 @@ def run_b200_arm(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        with torch.cuda.stream(engine_stream):
-            flush.zero_()
-        one_run()
-    barrier()
-    launches0 = net.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    signals = 0
-    result = None
-    with ClockSampler(local) as clocks:
-        ev0.record(engine_stream)
-        for _ in range(args.steps):
-            with torch.cuda.stream(engine_stream):
+    def max_over_ranks(x):
+        if world > 1:
+            t = torch.tensor([x], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            x = float(t.item())
+        return x
+
+    def timed_runs(net, steps, warmup, clock_gpu=None):
+        stream = torch.cuda.ExternalStream(net.stream_handle())
+        for _ in range(warmup):
+            with torch.cuda.stream(stream):
                 flush.zero_()
-            sig, conv, units, edges = one_run()
-            signals += sig
-            result = (sig, conv, units, edges)
-        ev1.record(engine_stream)
+            one_run(net)
         barrier()
-    launches = net.launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        l0 = net.launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        total = 0
+        res = None
+        clocks = ClockSampler(clock_gpu) if clock_gpu is not None else None
+        if clocks:
+            clocks.__enter__()
+        ev0.record(stream)
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            res = one_run(net)
+            total += res[0]
+        ev1.record(stream)
+        barrier()
+        if clocks:
+            clocks.__exit__(None, None, None)
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        return total, ms, res, net.launch_count() - l0, (clocks.summary() if clocks else None)
+
+    net = make_net("world" if world > 1 else None)
+    signals, ms, result, launches, clk = timed_runs(net, args.steps, args.warmup, local)
     value = signals / (ms * 1e-3)
-    clk = clocks.summary()
 
     # per-phase device time over one extra (untimed) run: the roofline's kernel
     trace = dict(pairs=0, processed=0, batches=0)
     phase = np.zeros(2, np.float64)
     _lib.check(lib.gs_engine_phase_ms(net.handle, 1, phase))
-    # step_device only records events when stats are harvested synchronously
-    one_run(trace)
+    x0 = net.exchange_ms()
+    one_run(net, trace)
     _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
     find_ms, update_ms = float(phase[0]), float(phase[1])
+    exch_ms = net.exchange_ms() - x0
     peaks = load_peaks()
+    sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fpeak, fpeak_src = fp32_peak(lib, ctx, sm_mhz, peaks)
     counts = net.counts()
     mean_deg = 2.0 * counts["edges"] / max(1, counts["units"])
-    if find_ms >= update_ms:
-        sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-        sms = _lib.default_context().sm_count
-        peak = 2 * 128 * sms * sm_mhz * 1e6 / 1e12
-        achieved = 8.0 * trace["pairs"] / (find_ms * 1e-3) / 1e12
-        roof = {"kernel": "find_exact_kernel", "bound": "fp32", "achieved": achieved,
-                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": ncu_traffic("find"),
-                "peak_source": f"nominal FP32 2x128 lanes x {sms} SMs at the sampled {sm_mhz:.0f} MHz",
-                "work": "8 FLOP per (signal, live unit) pair (BASELINE.md 2)",
-                "share_of_step": find_ms / (find_ms + update_ms)}
-    else:
-        per_sig = (1 + mean_deg) * 2 * (32 + 8) + mean_deg * (8 + 8) + 16 + 24
-        achieved = per_sig * trace["processed"] / (update_ms * 1e-3) / 1e9
-        peak = float(peaks.get("hbm_gbs", 6650.0))
-        roof = {"kernel": "k_update_batch", "bound": "hbm", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("update"),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else ""),
-                "work": f"{per_sig:.0f} B per processed signal (winner + {mean_deg:.2f} neighbours: "
-                        "pos+hab read/write, adjacency, edge ages, record, signal)",
-                "share_of_step": update_ms / (find_ms + update_ms),
-                "note": "sequential-semantics update on one 16-CTA cluster: bound by dependent L2 round trips and cluster barriers, not by bandwidth"}
+    total_phase = find_ms + exch_ms + update_ms
+    f_achieved = 8.0 * trace["pairs"] / world / (find_ms * 1e-3) / 1e12
+    find_roof = {"kernel": "find_small_f32_kernel (screened FP32 + exact FP64 candidates)",
+                 "bound": "fp32", "achieved": f_achieved, "peak": fpeak, "unit": "TFLOP/s",
+                 "frac": f_achieved / fpeak, "traffic": ncu_traffic("find"),
+                 "peak_source": fpeak_src,
+                 "work": "8 FLOP per (signal, live unit) pair (BASELINE.md 2) of this rank's slice",
+                 "share_of_step": find_ms / total_phase,
+                 "us_per_batch": 1e3 * find_ms / max(1, trace["batches"])}
+    per_sig = (1 + mean_deg) * 2 * (32 + 8) + mean_deg * (8 + 8) + 16 + 24
+    achieved = per_sig * trace["processed"] / (update_ms * 1e-3) / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roof = {"kernel": "k_update_batch", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic("update"),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else ""),
+            "work": f"{per_sig:.0f} B per processed signal (winner + {mean_deg:.2f} neighbours: "
+                    "pos+hab read/write, adjacency, edge ages, record, signal)",
+            "share_of_step": update_ms / total_phase,
+            "us_per_batch": 1e3 * update_ms / max(1, trace["batches"]),
+            "note": "sequential-semantics update on one 16-CTA cluster: bound by dependent L2 "
+                    "round trips and cluster barriers, not by bandwidth"}
+    if find_ms > update_ms:
+        roof, find_roof = find_roof, roof
 
-    # e2e through the public API: host sampling + H2D per batch + stats D2H
+    # e2e through the public API: cloud H2D + sampler state + stats inside
     e2e = None
     if not args.no_e2e:
         # one untimed pass through the public API (allocator / module warm-up)
@@ -644,7 +827,6 @@ def run_b200_arm(args):
         e_sig = e_batches = 0
         results = []  # the returned networks outlive the timed region (no teardown inside)
         for _ in range(args.steps):
-            t_run = time.perf_counter()
             if world > 1:
                 res_net, rs = run_multi_sharded(src, params, seed)
             else:
@@ -652,40 +834,79 @@ def run_b200_arm(args):
             results.append(res_net)
             e_sig += rs.signals
             e_batches += rs.iterations
-            if os.environ.get("GS_E2E_DEBUG"):
-                print(f"e2e run: {1e3 * (time.perf_counter() - t_run):.0f} ms "
-                      f"(loop {1e3 * rs.total_s:.0f} ms)", file=sys.stderr, flush=True)
         barrier()
-        e_s = time.perf_counter() - t0
+        e_s = max_over_ranks(time.perf_counter() - t0)
         del results
-        if world > 1:
-            t = torch.tensor([e_s], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_s = float(t.item())
         e2e = {"value": e_sig / e_s, "unit": "signals/s",
                "h2d_bytes_per_step": int(cloud_bytes + 48 + 120),
                "d2h_bytes_per_step": int(C.sizeof(_lib.GsBatchStats) * (e_batches // args.steps)),
                "ms_per_step": 1e3 * e_s / args.steps}
 
+    # N = 1: the sharded code path with a single-rank communicator (the SCALE
+    # anchor: same run, find + ncclAllGather + update per batch)
+    anchor = None
+    if world == 1 and not args.no_sharded_anchor:
+        net1 = make_net("world1")
+        a_sig, a_ms, _, a_l, _ = timed_runs(net1, max(1, min(args.steps, 3)), 1)
+        ph = np.zeros(2, np.float64)
+        _lib.check(lib.gs_engine_phase_ms(net1.handle, 1, ph))
+        x0 = net1.exchange_ms()
+        tr = dict(pairs=0, processed=0, batches=0)
+        one_run(net1, tr)
+        _lib.check(lib.gs_engine_phase_ms(net1.handle, 0, ph))
+        anchor = {"value": a_sig / (a_ms * 1e-3), "ms_per_step": a_ms / max(1, min(args.steps, 3)),
+                  "allgather_us_per_batch": 1e3 * (net1.exchange_ms() - x0) / max(1, tr["batches"]),
+                  "how": "same run through the sharded engine path at world = 1 (find on the "
+                         "rank's slice, ncclAllGather of records on the engine stream, update)"}
+        net1.close()
+
+    # BASELINE config 4: 10M-point torus, paper batch rule up to 65536, sharded
+    cfg4 = None
+    if not args.no_cfg4:
+        src4, params4, seed4, desc4 = workloads.make("cfg4")
+        kw = dict(capacity=65536)
+        run4 = (lambda: run_multi_sharded(src4, params4, seed4, **kw)) if world > 1 else (
+            lambda: run_multi(src4, params4, seed4, **kw))
+        run4()  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        net4, rs4 = run4()
+        barrier()
+        w_s = max_over_ranks(time.perf_counter() - t0)
+        loop_s = max_over_ranks(rs4.total_s)
+        x4 = net4.exchange_ms() if world > 1 else 0.0
+        cfg4 = {"desc": desc4, "cloud_points": int(src4.points.shape[0]), "signals": rs4.signals,
+                "batches": rs4.iterations, "units": rs4.units, "edges": rs4.connections,
+                "converged": rs4.converged, "wall_s": w_s, "loop_s": loop_s,
+                "signals_per_s": rs4.signals / loop_s, "signals_per_s_wall": rs4.signals / w_s,
+                "find_s": rs4.find_s, "update_s": rs4.update_s,
+                "allgather_us_per_batch": 1e3 * x4 / max(1, rs4.iterations),
+                "timing": "signals_per_s: the batch loop of the public run_multi call (per-batch "
+                          "host sampling of m, stats read each batch), max over ranks; "
+                          "signals_per_s_wall adds the cloud H2D and setup",
+                "parallelism": f"signal-sharded find x{world}, replicated update"}
+        net4.close()
+        del src4
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         wparams = dict(workloads.WORKLOADS[args.workload]["params"])
-        sig, sec, batches, kind, cores = reference_prefix(src.points, src.label, wparams, seed,
-                                                          args.cpu_budget_s)
-        cpu = {"value": sig / sec, "unit": "signals/s", "cores": cores, "kind": kind,
-               "sample": f"first {sig:,} signals ({batches} batches) of the same seeded "
-                         f"{args.workload} run ({sec:.1f} s)"}
+        v, c_ms, kind, cores, sample = reference_cpu_rate(src.points, src.label, wparams, seed,
+                                                          args.cpu_budget_s, args.workload)
+        cpu = {"value": v, "unit": "signals/s", "cores": cores, "kind": kind, "sample": sample,
+               "time_to_converge_s": c_ms * 1e-3}
+        if args.ref_full_cfg3 and reference_available():
+            cpu["full_run"] = reference_full_run(args.workload)
 
     sweep = None
     if rank == 0 and world == 1 and not args.no_m_sweep:
         sweep = m_sweep(lib, src, dict(workloads.WORKLOADS[args.workload]["params"]), seed)
     others = None
     if rank == 0 and world == 1 and not args.no_m_sweep:
-        others = other_configs(lib)
+        others = other_configs(lib, ref_full=not args.no_ref_full)
     fmb = None
     if rank == 0 and not args.no_find_microbench:
-        fmb = find_microbench(lib, _lib.default_context(),
-                              clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0), peaks)
+        fmb = find_microbench(lib, ctx, fpeak, fpeak_src)
 
     if rank == 0:
         sig, conv, units, edges = result
@@ -696,20 +917,25 @@ def run_b200_arm(args):
             "data": "synthetic",
             "config": {"workload": args.workload, "desc": desc, "m": m, "theta0": params.theta0,
                        "seed": seed, "cloud_points": int(src.points.shape[0]),
-                       "parallelism": f"signal-sharded find x{world}, replicated update",
+                       "parallelism": f"signal-sharded find x{world} (ncclAllGather of winner "
+                                      "records per batch), replicated update",
                        "step": "one seeded run from the two seed units to convergence",
                        "signals_per_step": sig, "converged": conv, "units": units,
                        "edges": edges, "time_to_converge_s": ms / args.steps * 1e-3,
                        "l2": "256 MiB L2 flush before each step (cloud "
                              f"{cloud_bytes / 2**20:.0f} MiB resident in HBM)",
-                       "sampling": "device Philox4x64-10 + Lemire, bit-identical to numpy",
+                       "sampling": "device Philox4x64-10 + Lemire inside the timed region, "
+                                   "bit-identical to numpy",
                        "find_mode": "auto"},
             "roofline": roof,
+            "find_roofline": find_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,
-            "phase_ms_per_step": {"find": find_ms, "update": update_ms},
+            "phase_ms_per_step": {"find": find_ms, "allgather": exch_ms, "update": update_ms},
+            "sharded_world1": anchor,
+            "cfg4": cfg4,
             "find_microbench": fmb,
             "m_sweep": sweep,
             "other_configs": others,

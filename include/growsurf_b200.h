@@ -53,6 +53,9 @@ gs_status gs_ctx_create(int device, gs_ctx **out);
 void gs_ctx_destroy(gs_ctx *ctx);
 /* Number of SMs of the context's device (grid sizing, roofline). */
 int gs_ctx_sm_count(const gs_ctx *ctx);
+/* Measured FP32 peak of the device: packed FFMA2 chains on every SM, best of
+ * 5 timed launches (TFLOP/s; *ms = that launch's time, may be NULL). */
+gs_status gs_fp32_peak(gs_ctx *ctx, double *tflops, double *ms);
 
 /* ------------------------------------------------------------------ */
 /* kernel-backend protocol: host buffers, synchronous                   */
@@ -194,7 +197,10 @@ gs_status gs_engine_resolve_host(gs_engine *eng, const double *signals, int64_t 
 #define GS_SHARD_ID_BYTES 128
 /* A fresh communicator id (rank 0 makes it, the caller broadcasts it). */
 gs_status gs_shard_unique_id(uint8_t *out, int64_t len);
-/* Join the world (blocks until every rank joined); world = 0 detaches. */
+/* Join the world (blocks until every rank joined); world = 0 detaches.
+ * Engines joined with the same id share one communicator (initialised by
+ * the first join, kept for the process); they must not run sharded steps
+ * concurrently. */
 gs_status gs_engine_set_shards(gs_engine *eng, int world, int rank, const uint8_t *id,
                                int64_t len);
 /* Device time of the record all-gathers (with phase timing on), ms. */

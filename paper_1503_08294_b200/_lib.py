@@ -57,6 +57,7 @@ _SIGNATURES = {
     "gs_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "gs_ctx_destroy": (None, [_vp]),
     "gs_ctx_sm_count": (C.c_int, [_vp]),
+    "gs_fp32_peak": (C.c_int, [_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "gs_best_two_single": (C.c_int, [_vp, _f64p, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                      C.c_double, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),

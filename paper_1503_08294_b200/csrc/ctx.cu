@@ -140,3 +140,55 @@ extern "C" void gs_ctx_destroy(gs_ctx* ctx) {
 }
 
 extern "C" int gs_ctx_sm_count(const gs_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+
+// ---------------------------------------------------------------------------
+// FP32 peak probe (the find roofline's denominator, measured on the box):
+// every thread runs 8 independent chains of packed FFMA2 (2 FMA = 4 FLOP
+// each); one CTA of 512 threads per SM slot, 4 per SM.
+
+namespace {
+__global__ void __launch_bounds__(512) k_ffma2_peak(float* out, int iters, float seed) {
+  float2 a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    a[k] = make_float2(seed * (threadIdx.x + k), seed * (blockIdx.x + k));
+  const float2 b = make_float2(0.9999999f, 1.0000001f), c = make_float2(1e-7f, -1e-7f);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __ffma2_rn(a[k], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k].x + a[k].y;
+  if (s == 1234.5f) out[0] = s;  // never true; keeps the chains alive
+}
+}  // namespace
+
+extern "C" gs_status gs_fp32_peak(gs_ctx* ctx, double* tflops, double* ms) {
+  return guarded([&] {
+    GS_CHECK(ctx && tflops, GS_VALUE_ERROR, "null argument");
+    GS_CUDA(cudaSetDevice(ctx->device));
+    float* out = (float*)ctx->ensure_device(sizeof(float));
+    const int blocks = 4 * ctx->sm_count, threads = 512, iters = 1 << 15;
+    cudaEvent_t e0, e1;
+    GS_CUDA(cudaEventCreate(&e0));
+    GS_CUDA(cudaEventCreate(&e1));
+    k_ffma2_peak<<<blocks, threads, 0, ctx->stream>>>(out, 256, 1e-3f);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      GS_CUDA(cudaEventRecord(e0, ctx->stream));
+      k_ffma2_peak<<<blocks, threads, 0, ctx->stream>>>(out, iters, 1e-3f);
+      GS_CUDA(cudaEventRecord(e1, ctx->stream));
+      GS_CUDA(cudaEventSynchronize(e1));
+      float t = 0.f;
+      GS_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      best = t < best ? t : best;
+    }
+    GS_CUDA(cudaGetLastError());
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flop = 4.0 * 8.0 * (double)iters * blocks * threads;
+    *tflops = flop / (best * 1e-3) / 1e12;
+    if (ms) *ms = best;
+  });
+}

@@ -45,6 +45,9 @@
 #include <cmath>
 #include <cstring>
 #include <vector>
+#include <map>
+#include <mutex>
+#include <string>
 
 #include <cooperative_groups.h>
 #include <nccl.h>
@@ -1265,7 +1268,6 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
     cudaStreamSynchronize(e->side);
     cudaStreamDestroy(e->side);
   }
-  if (e->comm) ncclCommDestroy(e->comm);
   for (int h = 0; h < 2; ++h) {
     if (e->pf_done[h]) cudaEventDestroy(e->pf_done[h]);
     if (e->use_done[h]) cudaEventDestroy(e->use_done[h]);
@@ -1663,6 +1665,16 @@ extern "C" gs_status gs_shard_unique_id(uint8_t* out, int64_t len) {
   });
 }
 
+namespace {
+// communicators by (id, world, rank): every engine joined with the same id
+// shares one (a run's Network, the next run's Network ...), so only the
+// first join pays ncclCommInitRank.  Kept for the life of the process;
+// engines sharing one must not run sharded steps concurrently (the
+// collectives of one communicator are issued in one order on every rank).
+std::mutex g_comm_mu;
+std::map<std::string, ncclComm_t> g_comms;
+}  // namespace
+
 extern "C" gs_status gs_engine_set_shards(gs_engine* e, int world, int rank, const uint8_t* id,
                                           int64_t len) {
   return guarded([&] {
@@ -1670,22 +1682,28 @@ extern "C" gs_status gs_engine_set_shards(gs_engine* e, int world, int rank, con
     GS_CHECK(world >= 0 && (world == 0 || (0 <= rank && rank < world)), GS_VALUE_ERROR,
              "bad world / rank");
     GS_CUDA(cudaStreamSynchronize(e->stream));
-    if (e->comm) {
-      ncclCommDestroy(e->comm);
-      e->comm = nullptr;
-    }
+    e->comm = nullptr;
     e->world = 1;
     e->rank = 0;
     if (world == 0) return;
     GS_CHECK(id && len == (int64_t)sizeof(ncclUniqueId), GS_VALUE_ERROR,
              "the shard id must be GS_SHARD_ID_BYTES long");
-    ncclUniqueId uid;
-    memcpy(&uid, id, sizeof(uid));
-    GS_CUDA(cudaSetDevice(e->ctx->device));
-    ncclComm_t comm = nullptr;
-    const ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
-    GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-    e->comm = comm;
+    std::string key((const char*)id, (size_t)len);
+    key += "/" + std::to_string(world) + "/" + std::to_string(rank) + "/" +
+           std::to_string(e->ctx->device);
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    auto it = g_comms.find(key);
+    if (it == g_comms.end()) {
+      ncclUniqueId uid;
+      memcpy(&uid, id, sizeof(uid));
+      GS_CUDA(cudaSetDevice(e->ctx->device));
+      ncclComm_t comm = nullptr;
+      const ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
+      GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR,
+               std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      it = g_comms.emplace(key, comm).first;
+    }
+    e->comm = it->second;
     e->world = world;
     e->rank = rank;
   });

@@ -54,13 +54,22 @@ def broadcast_shard_id(group=None, make_id=shard_unique_id) -> bytes:
     return uid
 
 
+_GROUP_IDS: dict = {}  # group -> communicator id (the engine reuses its communicator)
+
+
 def attach(net, group=None) -> tuple[int, int]:
     """Join ``net`` to the ranks of ``group`` (blocks until all joined);
-    returns (world, rank)."""
+    returns (world, rank).  The first call per group broadcasts a fresh
+    communicator id; later calls (the next run's Network) reuse it, so the
+    NCCL communicator is initialised once per process and group."""
     import torch.distributed as dist
 
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    net.set_shards(world, rank, broadcast_shard_id(group))
+    key = id(group if group is not None else dist.group.WORLD)
+    uid = _GROUP_IDS.get(key)
+    if uid is None:
+        uid = _GROUP_IDS[key] = broadcast_shard_id(group)
+    net.set_shards(world, rank, uid)
     return world, rank
 
 

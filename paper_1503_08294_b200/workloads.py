@@ -30,6 +30,12 @@ def double_torus_cloud(n: int = 1_000_000):
     return DoubleTorusSource().sample(np.random.Generator(np.random.Philox(2026)), n)
 
 
+@functools.lru_cache(maxsize=None)
+def torus_10m_cloud(n: int = 10_000_000):
+    """Config 4 input: n points on the (2.0, 0.5) torus from Philox(2026)."""
+    return TorusSource(2.0, 0.5).sample(np.random.Generator(np.random.Philox(2026)), n)
+
+
 WORKLOADS = {
     # BASELINE config 3: SOAM on a 1M-point genus-2 cloud.  theta0 = 0.1 and
     # m = 4096 were calibrated so the (bit-identical) run converges to a
@@ -38,6 +44,19 @@ WORKLOADS = {
         desc="SOAM, 1M-point synthetic genus-2 cloud (two-torus blend), m=4096, theta0=0.1",
         cloud=lambda: (double_torus_cloud(), "double-torus-1M"),
         params=dict(theta0=0.1, batch_floor=4096, batch_cap=4096, max_signals=60_000_000),
+        seed=7,
+    ),
+    # BASELINE config 4: multi-signal GNG on a 10M-point cloud, the paper's
+    # batch rule up to m = 65536 (m = smallest power of two above V; reached
+    # once V > 32768, ~batch 172), signals sharded across 1/2/4/8 GPUs.  A
+    # fixed signal budget (the network keeps growing: V ~ 38k at 2.3 M
+    # signals); tests/golden/run_cfg4_prefix.npz is the reference's first
+    # 4 M signals.
+    "cfg4": dict(
+        desc="GNG multi-signal, 10M-point synthetic torus cloud, m up to 65536 (paper rule), "
+             "theta0=0.025",
+        cloud=lambda: (torus_10m_cloud(), "torus-10M"),
+        params=dict(theta0=0.025, batch_cap=65536, max_signals=30_000_000),
         seed=7,
     ),
     # BASELINE config 2 working anchor: converges V=681.

@@ -52,6 +52,8 @@ CASES = {
     # find, the n <= 6144 FP64 small find and the grid
     "v8k": dict(source=("cloud", "torus100k"), seed=7,
                 params=dict(theta0=0.05, batch_cap=8192, max_signals=1_500_000)),
+    "cfg4_prefix": dict(source=("cloud", "torus10M"), seed=7,
+                        params=dict(theta0=0.025, batch_cap=65536, max_signals=4_000_000)),
     "v8k_fixed": dict(source=("cloud", "torus100k"), seed=7,
                       params=dict(theta0=0.05, batch_floor=8192, batch_cap=8192,
                                   max_signals=1_228_800)),
@@ -66,6 +68,10 @@ def make_source(spec):
         return TorusSource(spec[1], spec[2])
     if kind == "cloud":
         sph, tor = clouds()
+        if spec[1] == "torus10M":
+            from paper_1503_08294_b200.workloads import torus_10m_cloud
+
+            return CloudSource(torus_10m_cloud(), label=spec[1])
         pts = {"sphere10k": sph, "torus100k": tor, "hemisphere": hemisphere_cloud()}[spec[1]]
         return CloudSource(pts, label=spec[1])
     raise ValueError(spec)

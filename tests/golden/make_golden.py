@@ -82,6 +82,10 @@ CASES = {
     # the paper batch rule (m up to 8192); V ~ 9.9k after 1.5 M signals
     "v8k": dict(source=("cloud", "torus100k"), seed=7,
                 params=dict(theta0=0.05, batch_cap=8192, max_signals=1_500_000)),
+    # BASELINE config 4 prefix: 10M-point torus cloud, paper batch rule up to
+    # m = 65536 (paper_1503_08294_b200/workloads.py "cfg4"), first ~4 M signals
+    "cfg4_prefix": dict(source=("cloud", "torus10M"), seed=7, parallel=True,
+                        params=dict(theta0=0.025, batch_cap=65536, max_signals=4_000_000)),
     # the same cloud with a fixed m = 8192 (the asynchronous device-sampled path)
     "v8k_fixed": dict(source=("cloud", "torus100k"), seed=7,
                       params=dict(theta0=0.05, batch_floor=8192, batch_cap=8192,
@@ -89,8 +93,15 @@ CASES = {
 }
 
 
+def torus10m_cloud():
+    """BASELINE config 4's 10M-point torus cloud (workloads.py torus_10m_cloud)."""
+    return TorusSource(2.0, 0.5).sample(np.random.Generator(np.random.Philox(2026)), 10_000_000)
+
+
 def make_source(spec, cache):
     kind = spec[0]
+    if kind == "cloud" and spec[1] == "torus10M" and spec[1] not in cache:
+        cache[spec[1]] = torus10m_cloud()
     if kind == "sphere":
         return SphereSource(spec[1])
     if kind == "torus":
@@ -100,7 +111,7 @@ def make_source(spec, cache):
     raise ValueError(spec)
 
 
-def trace_run(source, params: EngineParams, seed: int):
+def trace_run(source, params: EngineParams, seed: int, executor=None):
     """The run_multi driver (multi.py:134-185) with the state kept visible."""
     rng = np.random.Generator(np.random.Philox(seed))
     net = Network()
@@ -111,7 +122,7 @@ def trace_run(source, params: EngineParams, seed: int):
     digest = hashlib.sha256()
     digest.update(np.ascontiguousarray(seeds).tobytes())
     state = RunState()
-    executor = sequential_executor()
+    executor = executor or sequential_executor()
     per_batch = []
     signals = discarded = iterations = 0
     converged = False
@@ -189,7 +200,12 @@ def main(only=None):
         params = EngineParams(**case["params"])
         src = make_source(case["source"], cache)
         t0 = time.perf_counter()
-        net, state, per_batch, digest, stats = trace_run(src, params, case["seed"])
+        ex = None
+        if case.get("parallel"):  # bitwise identical to the sequential scan (test_multi.py:180-192)
+            from growsurf.parallel import ExecConfig, parallel_executor
+
+            ex = parallel_executor(ExecConfig(workers=os.cpu_count() or 1))
+        net, state, per_batch, digest, stats = trace_run(src, params, case["seed"], ex)
         dt = time.perf_counter() - t0
         # cross-check the traced driver against the reference's own run_multi
         if name in ("sphere_exec", "cfg1", "stress", "boundary"):

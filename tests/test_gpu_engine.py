@@ -40,8 +40,8 @@ def test_device_run_matches_reference_golden(name):
     net.audit()
 
 
-@pytest.mark.parametrize("name", ["v8k", "v8k_fixed"])
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])  # exact, filter, AUTO, screened small, grid
+@pytest.mark.parametrize("name,mode", [(n, k) for n in ("v8k", "v8k_fixed") for k in range(5)]
+                         + [("cfg4_prefix", k) for k in (1, 2, 4)])
 def test_large_network_find_modes_match_reference(name, mode):
     """V grows past 4096 (to ~9.9k): the engine's find leaves the screened
     small kernel (n <= 4096) for the FP64 small kernel (n <= 6144), the
@@ -276,7 +276,8 @@ def test_cfg3_headline_run_matches_reference():
     assert manifold_check(mesh) == "closed" and genus(mesh) == 2
 
 
-@pytest.mark.parametrize("name", ["paper_rule", "boundary", "cfg1", "v8k", "v8k_fixed"])
+@pytest.mark.parametrize("name", ["paper_rule", "boundary", "cfg1", "v8k", "v8k_fixed",
+                                  "cfg4_prefix"])
 def test_run_multi_device_sampling_matches_golden(name):
     """run_multi on a CloudSource draws its batches on the device (variable m
     under the paper's batch rule: synchronous; fixed m: the asynchronous

@@ -50,7 +50,7 @@ def _check_stats(st, gold):
         assert int(getattr(st, k)) == int(gold[f"stat_{k}"]), k
 
 
-@pytest.mark.parametrize("name", ["cfg1", "stress", "paper_rule", "v8k_fixed"])
+@pytest.mark.parametrize("name", ["cfg1", "stress", "paper_rule", "v8k_fixed", "cfg4_prefix"])
 def test_run_multi_sharded_world1_matches_golden(world1, name):
     from paper_1503_08294_b200 import EngineParams
     from paper_1503_08294_b200.distributed import run_multi_sharded
@@ -120,8 +120,8 @@ def test_set_shards_without_torch_distributed():
     net.set_shards(0, 0)  # detach
 
 
-@pytest.mark.parametrize("k", [2, 4])
-@pytest.mark.parametrize("name", ["cfg1", "stress", "v8k"])
+@pytest.mark.parametrize("name,k", [(n, k) for n in ("cfg1", "stress", "v8k") for k in (2, 4)]
+                         + [("cfg4_prefix", 8)])
 def test_k_shard_split_on_one_gpu_matches_golden(name, k):
     import torch
 
