@@ -61,10 +61,15 @@ def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, back
     loop with a batch of one (the winner lock never triggers), so it runs on
     the same device engine and matches the reference run bit for bit.
     ``checkpoints`` records (units, signals, sample_s, find_s, update_s,
-    total_s) the first time the unit count reaches each value.  The
-    reference's hash grid (use_grid=True, grid.py:98-133) is approximate and
-    has no exact parity target; the exact device grid (GS_FIND_GRID) serves
-    the batched find, where its per-call build is amortised.
+    total_s) the first time the unit count reaches each value.
+
+    ``use_grid=True`` is the reference's "indexed" variant (engine.py:396-426,
+    grid.py:98-133): the winner search goes through a spatial grid instead of
+    the exhaustive scan.  Here that grid is the device's EXACT uniform grid
+    (GS_FIND_GRID, rebuilt on the device per find), so the indexed run equals
+    the exhaustive run bit for bit -- unlike the reference's approximate
+    HashGrid, whose winners may differ; its parity target
+    is therefore the exhaustive run.
     """
     import ctypes as C
     import time
@@ -73,14 +78,10 @@ def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, back
     from . import _lib
     from .metrics import RunStats
 
-    if use_grid:
-        raise ValueError("the approximate hash-grid (indexed) variant is not provided; "
-                         "use_grid=False runs the exact single-signal engine (the exact "
-                         "device grid serves batched finds: find_mode=FIND_GRID)")
     lib = _lib.load_library()
     p1 = replace(params, batch_floor=1, batch_cap=1)
     rng = np.random.Generator(np.random.Philox(seed))
-    net = Network(p1)
+    net = Network(p1, find_mode=_lib.FIND_GRID if use_grid else _lib.FIND_AUTO)
     net.watch_age_limit(params.max_age)
     seeds = source.sample(rng, 2)
     for k in range(2):
@@ -112,7 +113,7 @@ def run(source, params: EngineParams, seed: int, *, use_grid: bool = False, back
     total = perf() - t_start
     _lib.check(lib.gs_engine_phase_ms(net.handle, 0, phase))
     net._touch()
-    stats = RunStats(variant=variant or "single", dataset=dataset or getattr(source, "label", "unknown"),
+    stats = RunStats(variant=variant or ("indexed" if use_grid else "single"), dataset=dataset or getattr(source, "label", "unknown"),
                      seed=seed, iterations=signals, signals=signals, discarded=0,
                      units=int(st.units), connections=int(st.edges), total_s=total,
                      sample_s=sample_s, find_s=phase[0] * 1e-3, update_s=phase[1] * 1e-3,

@@ -173,8 +173,29 @@ def test_single_signal_run_matches_reference():
     assert np.array_equal(got["ids"], gold["ids"]) and np.array_equal(got["edges"], gold["edges"])
     for k in ("pos", "hab", "theta"):
         assert np.array_equal(got[k].view(np.int64), gold[k].view(np.int64)), k
-    with pytest.raises(ValueError):
-        run(SphereSource(1.0), EngineParams(max_signals=10), 3, use_grid=True)
+
+
+@pytest.mark.gpu
+def test_indexed_run_equals_exhaustive_reference_run():
+    """run(use_grid=True), the "indexed" variant (engine.py:396-426): the
+    winner search goes through the device's exact grid, so the run equals
+    the reference's exhaustive single-signal run bit for bit (the
+    reference's own HashGrid is approximate)."""
+    from paper_1503_08294_b200 import EngineParams, SphereSource, run
+
+    gold = load_golden("single")
+    if not same_numpy(gold):
+        pytest.skip("golden made with another numpy")
+    net, st = run(SphereSource(1.0), EngineParams(theta0=0.35, max_signals=20_000), 3,
+                  use_grid=True, checkpoints=(10, 40))
+    assert st.variant == "indexed"
+    for k in ("iterations", "signals", "units", "connections", "converged"):
+        assert int(getattr(st, k)) == int(gold[f"stat_{k}"]), k
+    assert [c[1] for c in st.checkpoints] == list(gold["checkpoint_signals"])
+    got = net.export()
+    assert np.array_equal(got["ids"], gold["ids"]) and np.array_equal(got["edges"], gold["edges"])
+    for k in ("pos", "hab", "theta"):
+        assert np.array_equal(got[k].view(np.int64), gold[k].view(np.int64)), k
 
 
 @pytest.mark.gpu
