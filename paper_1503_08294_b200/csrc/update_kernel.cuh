@@ -45,6 +45,28 @@ __device__ __forceinline__ void stage_adj(const int2* A, int d, int2 (&nb)[kStag
   }
 }
 
+#ifndef GS_OPT_STAGEALL_B
+#define GS_OPT_STAGEALL_B 0
+#endif
+#ifndef GS_OPT_STAGEALL_W
+#define GS_OPT_STAGEALL_W 0
+#endif
+#ifndef GS_OPT_HAB_B
+#define GS_OPT_HAB_B 0
+#endif
+// the first kStage slots of a row regardless of the degree (rows hold kMaxDeg
+// slots, so the loads never leave the row): they issue together with the
+// degree load instead of after it; callers ignore slots past the degree
+__device__ __forceinline__ void stage_adj_all(const int2* A, int2 (&nb)[kStage]) {
+  const int4* A4 = reinterpret_cast<const int4*>(A);
+#pragma unroll
+  for (int k = 0; k < kStage / 2; ++k) {
+    const int4 v = A4[k];
+    nb[2 * k] = make_int2(v.x, v.y);
+    nb[2 * k + 1] = make_int2(v.z, v.w);
+  }
+}
+
 __device__ __forceinline__ void replay_event(double4& p, double& h, const Params& P,
                                              const double* sig, int key) {
   const size_t j = (size_t)(key >> 1);
@@ -61,33 +83,40 @@ __device__ __forceinline__ void replay_event(double4& p, double& h, const Params
 // replay unit u's updates from the committed signals (< jstar) of this window
 // in batch order: keys (j << 1) | self are unique (a signal has one winner),
 // so "smallest key above the last one" walks them in order without sorting.
-__device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
-                          int jstar) {
+// Computes without storing: p / h are u's values after the replay, the
+// return value the largest signal index replayed (-1: none, u unchanged).
+__device__ int walk_compute(const DevState& S, const Params& P, const double* sig, int u,
+                            int jstar, double4& p, double& h) {
   const int2* A = S.adj + (size_t)u * kMaxDeg;
   const int d = S.deg[u];
   const int jself = S.firstwin[u];
-  double4 p = S.pos[u];
-  const double h0 = S.hab[u];
-  double h = h0;
+  p = S.pos[u];
+  h = S.hab[u];
   constexpr int kNone = 0x7fffffff;
+  int last = -1;
   if (d <= 2 * kStage) {
     // up to 2*kStage neighbours: keys staged in registers, two chunks of loads
     constexpr int kK = 2 * kStage;
     int key[kK + 1];
+    int2 nb[2][kStage];
+#if GS_OPT_STAGEALL_W
+    stage_adj_all(A, nb[0]);
+    stage_adj_all(A + kStage, nb[1]);
+#else
+    stage_adj(A, min(kStage, d), nb[0]);
+    stage_adj(A + kStage, d - kStage, nb[1]);
+#endif
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      int2 nb[kStage];
       const int dc = min(kStage, d - c * kStage);
-      stage_adj(A + c * kStage, dc, nb);
 #pragma unroll
       for (int k = 0; k < kStage; ++k) {
-        const int jw = k < dc ? S.firstwin[nb[k].x] : kNone;
+        const int jw = k < dc ? S.firstwin[nb[c][k].x] : kNone;
         key[c * kStage + k] = jw < jstar ? (jw << 1) : kNone;
       }
     }
     key[kK] = jself < jstar ? ((jself << 1) | 1) : kNone;
     // four events per group: their signal loads issue together
-    int last = -1;
 #pragma unroll 1
     for (int grp = 0; grp < (kK + 4) / 4; ++grp) {
       int cur[4];
@@ -123,7 +152,6 @@ __device__ void walk_unit(const DevState& S, const Params& P, const double* sig,
       if (cur[3] == kNone) break;
     }
   } else {
-    int last = -1;
     while (true) {
       int cur = (jself < jstar && ((jself << 1) | 1) > last) ? ((jself << 1) | 1) : kNone;
       for (int k = 0; k < d; ++k) {
@@ -136,9 +164,67 @@ __device__ void walk_unit(const DevState& S, const Params& P, const double* sig,
       last = cur;
     }
   }
+  return last < 0 ? -1 : (last >> 1);
+}
+
+// store a walked unit (h0: its habituation before the replay)
+__device__ __forceinline__ void walk_store(const DevState& S, const Params& P, int u,
+                                           const double4& p, double h, double h0) {
   S.pos[u] = p;
   S.hab[u] = h;
   if (h0 >= P.h_t && h < P.h_t) atomicSub(&S.cnt->untrained, 1);
+}
+
+__device__ void walk_unit(const DevState& S, const Params& P, const double* sig, int u,
+                          int jstar) {
+  double4 p;
+  double h;
+  const double h0 = S.hab[u];
+  if (walk_compute(S, P, sig, u, jstar, p, h) >= 0) walk_store(S, P, u, p, h, h0);
+}
+
+// one chunk of the winner b's adjacency for B: the event tests (b-s edge
+// exists, an edge crossing max_age) and, per entry, the C1 edge-age replay
+// value (age after this signal) and the neighbour's first processed signal,
+// all against the window-start state
+struct BScan {
+  bool found;
+  bool ev;
+  int kcn;
+};
+__device__ __forceinline__ void b_chunk(const DevState& S, const Params& P,
+                                        const WinRec* __restrict__ rec, int b, int s, int jj,
+                                        bool b_trained, const int2 (&nb)[kStage], int dc,
+                                        int (&na)[kStage], int (&jvo)[kStage], BScan& acc) {
+  int age[kStage], jv[kStage];
+#pragma unroll
+  for (int k = 0; k < kStage; ++k) {
+    const bool valid = k < dc;
+    age[k] = valid ? S.eage[nb[k].y] : 0;
+    jv[k] = valid ? S.firstwin[nb[k].x] : kNone32;
+  }
+  int sv[kStage];
+#pragma unroll
+  for (int k = 0; k < kStage; ++k) sv[k] = (k < dc && jv[k] < jj) ? rec[jv[k]].s : -1;
+#pragma unroll
+  for (int k = 0; k < kStage; ++k) {
+    jvo[k] = jv[k];
+    na[k] = 0;
+    if (k >= dc) continue;
+    const bool is_s = nb[k].x == s;
+    acc.found |= is_s;
+    const bool age_risk = !is_s && age[k] + 2 > P.max_age;
+    if (!b_trained || age_risk) {
+      if (jv[k] < jj) acc.kcn++;
+      if (age_risk) {
+        const int a2 = jv[k] < jj ? ((sv[k] == b) ? 0 : age[k] + 1) : age[k];
+        if (a2 + 1 > P.max_age) acc.ev = true;
+      }
+    }
+    int a = age[k];
+    if (jv[k] < jj) a = (sv[k] == b) ? 0 : a + 1;
+    na[k] = is_s ? 0 : a + 1;
+  }
 }
 
 __device__ __forceinline__ double pow_chain(double h, double c, int k) {
@@ -531,68 +617,65 @@ __device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, 
   return __shfl_sync(0xffffffffu, fired, 0);
 }
 
-// adapt_threshold outcome (engine.py:208-265) of committed signal jj with
-// winner b, from the window-start state: -2 none, else patience | shrink << 30.
-// Evaluated in C1 (not B): it never makes an event, so it stays off B's
-// critical path and overlaps C1's own loads.
-__device__ int adapt_outcome(const DevState& S, const Params& P, int b, int jj, bool hb_low) {
-  const int ringb = S.ring[b], patb = S.patience[b];
-  const int db = S.deg[b];
-  const int2* B = S.adj + (size_t)b * kMaxDeg;
-  int pat = -2;
-  if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) {
-    pat = 0;
-  } else if (hb_low) {
-    // every neighbour must be trained at time jj (engine.py:225-231):
-    // neighbours' habituation loads issue together per chunk; only the
-    // untrained-at-window-start ones need their decays replayed
-    bool ok = true;
-    for (int c0 = 0; c0 < db && ok; c0 += kStage) {
-      const int dc = min(kStage, db - c0);
-      int2 nb[kStage];
-      stage_adj(B + c0, dc, nb);
-      double hv0[kStage];
+// habituation of neighbour v (untrained at the window start, hvT) at the
+// time of signal jj: its decays from the window's signals before jj replayed
+// (as a neighbour of their winners, and once as a winner itself)
+__device__ __noinline__ double hab_at(const DevState& S, const Params& P, int v, double hvT,
+                                      int jj) {
+  const int jv = S.firstwin[v];
+  const bool vwon = jv < jj;
+  const int dv = S.deg[v];
+  const int2* V = S.adj + (size_t)v * kMaxDeg;
+  int k1 = 0, k2 = 0;
+  for (int q0 = 0; q0 < dv; q0 += kStage) {
+    const int dq = min(kStage, dv - q0);
+    int2 wb[kStage];
+    stage_adj(V + q0, dq, wb);
+    int jw[kStage];
 #pragma unroll
-      for (int k = 0; k < kStage; ++k) hv0[k] = k < dc ? S.hab[nb[k].x] : 0.0;
-#pragma unroll 1
-      for (int k = 0; k < dc && ok; ++k) {
-        const double hvT = hv0[k];
-        if (hvT < P.h_t) continue;
-        const int v = nb[k].x;
-        const int jv = S.firstwin[v];
-        const bool vwon = jv < jj;
-        const int dv = S.deg[v];
-        const int2* V = S.adj + (size_t)v * kMaxDeg;
-        int k1 = 0, k2 = 0;
-        for (int q0 = 0; q0 < dv; q0 += kStage) {
-          const int dq = min(kStage, dv - q0);
-          int2 wb[kStage];
-          stage_adj(V + q0, dq, wb);
-          int jw[kStage];
+    for (int q = 0; q < kStage; ++q) jw[q] = q < dq ? S.firstwin[wb[q].x] : kNone32;
 #pragma unroll
-          for (int q = 0; q < kStage; ++q) jw[q] = q < dq ? S.firstwin[wb[q].x] : kNone32;
-#pragma unroll
-          for (int q = 0; q < kStage; ++q) {
-            if (q < dq && jw[q] <= jj) {
-              if (vwon && jw[q] > jv) k2++;
-              else k1++;
-            }
-          }
-        }
-        double hv = pow_chain(hvT, P.c_n, k1);
-        if (vwon) hv = dmul(hv, P.c_b);
-        hv = pow_chain(hv, P.c_n, k2);
-        if (hv >= P.h_t) ok = false;
+    for (int q = 0; q < kStage; ++q) {
+      if (q < dq && jw[q] <= jj) {
+        if (vwon && jw[q] > jv) k2++;
+        else k1++;
       }
     }
-    if (ok) {
-      int cnt = patb + 1;
-      const int shrink = cnt >= P.ring_patience ? 1 : 0;
-      if (shrink) cnt = 0;
-      pat = cnt | (shrink << 30);
-    }
   }
-  return pat;
+  double hv = pow_chain(hvT, P.c_n, k1);
+  if (vwon) hv = dmul(hv, P.c_b);
+  return pow_chain(hv, P.c_n, k2);
+}
+
+// adapt_threshold outcome (engine.py:208-265) of signal jj with winner b
+// (degree db <= 2 * kStage, adjacency staged in nb0 / nb1; bit k of untr:
+// neighbour k untrained at the window start), from the window-start state:
+// -2 none, else patience | shrink << 30
+__device__ __forceinline__ int adapt_outcome_staged(const DevState& S, const Params& P, int jj,
+                                                    bool hb_low, int ringb, int patb, int db,
+                                                    const int2 (&nb0)[kStage],
+                                                    const int2 (&nb1)[kStage], unsigned untr) {
+  if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) return 0;
+  if (!hb_low) return -2;
+  // every neighbour must be trained at time jj (engine.py:225-231); only the
+  // untrained-at-window-start ones need their decays replayed
+  bool ok = true;
+#pragma unroll 1
+  for (; untr && ok; untr &= untr - 1) {
+    const int k = __ffs(untr) - 1;
+    int v = -1;
+#pragma unroll
+    for (int q = 0; q < kStage; ++q) {
+      v = q == k ? nb0[q].x : v;
+      v = kStage + q == k ? nb1[q].x : v;
+    }
+    if (hab_at(S, P, v, S.hab[v], jj) >= P.h_t) ok = false;
+  }
+  if (!ok) return -2;
+  int cnt = patb + 1;
+  const int shrink = cnt >= P.ring_patience ? 1 : 0;
+  if (shrink) cnt = 0;
+  return cnt | (shrink << 30);
 }
 
 // ---------------------------------------------------------------------------
@@ -753,9 +836,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   long long tick0 = 0, minla = 0;
   bool cand = false;
   int cb = -1;
+  int my_s = -1;      // this thread's record (second, d_winner): kept from A
+  double my_dw = 0.0;
   bool my_proc = false;  // this thread's window signal is processed ...
   int my_rank = 0, my_j = 0;  // ... at this rank
-  bool my_hblow = false;
   int my_abs = 0;
   while (j0 < m) {
     if (lead) t_ph = clock64();
@@ -771,6 +855,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (j < wend) {
         const WinRec r = rec[j];
         cb = r.b;
+        my_s = r.s;
+        my_dw = r.dwin;
         cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
                S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
         if (cand) atomicMin(&S.firstwin[r.b], j);
@@ -797,71 +883,91 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     const long long next_sweep = c->next_sweep;
     const int n_units = c->n_units;
     const bool iso = c->iso_count > 0;
-    // ---- B: events and adapt_threshold outcomes; each processed signal on
-    //      the thread that found it in A
+    // ---- B: events, and everything C1 and the walk need, read once against
+    //      the window-start state before the cluster reduction: each
+    //      processed signal on the thread that found it in A computes its
+    //      event tests, its adapt_threshold outcome and its edge-age replay
+    //      values; every thread replays its own unit slot as if the whole
+    //      segment commits.  After the reduction only stores remain (the
+    //      reads of C1 and the walk no longer follow one another, so the
+    //      barrier between them is gone).
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     long long evkey = 0x7fffffffffffffffLL;  // (rank << 32) | signal of this thread's event
+    int c1_pat = -2;                         // adapt_threshold outcome (adapt_outcome)
+    int c1_d = 0;                            // winner degree (<= 2 * kStage)
+    int2 c1_nb0[kStage], c1_nb1[kStage];     // its adjacency ...
+    int c1_a0[kStage], c1_a1[kStage];        // ... edge ages after this signal ...
+    int c1_j0[kStage], c1_j1[kStage];        // ... and the neighbours' first signals
+    const int nid_b = c->next_id;
     if (my_proc && my_rank >= rbase) {
       const int r = my_rank;
       const int jj = my_j;
-      const WinRec w = rec[jj];
-      const int b = w.b, s = w.s;
+      const int b = cb, s = my_s;
       const long long tick_j = tick0 + r + 1;
       bool ev = iso;
       if (tick_j >= next_sweep && ((tick_j - next_sweep) % kSweepEvery) == 0) {
         const long long cutoff = tick_j - horizon;
         if (cutoff > 0 && (minla < cutoff || n_units <= 2)) ev = true;
       }
-      const int db = S.deg[b];
+      // one load level for the winner's row, degree and scalars; the next
+      // for its neighbours (edge ages, first signals, habituation)
       const int2* B = S.adj + (size_t)b * kMaxDeg;
+      const int db = S.deg[b];
+#if GS_OPT_STAGEALL_B
+      stage_adj_all(B, c1_nb0);
+      stage_adj_all(B + kStage, c1_nb1);
+#else
+      stage_adj(B, min(kStage, db), c1_nb0);
+      stage_adj(B + kStage, db - kStage, c1_nb1);
+#endif
       // habituation only decays, so a unit trained at the window start stays
       // trained: exact per-time values are replayed only for untrained units
       const double hbT = S.hab[b];
       const double thb = S.theta[b];
+      const int ringb = S.ring[b], patb = S.patience[b];
       const long long la_b = S.la_val[b], la_s = S.la_val[s];
       const bool b_trained = hbT < P.h_t;
-      bool found = false;
-      int kcn = 0;
-      // the adjacency in chunks of kStage entries: each chunk's loads issue
-      // together (any degree, no dependent per-entry chains)
-      for (int c0 = 0; c0 < db; c0 += kStage) {
-        const int dc = min(kStage, db - c0);
-        int2 nb[kStage];
-        stage_adj(B + c0, dc, nb);
-        int age[kStage], jv[kStage];
+      BScan acc{false, false, 0};
+      unsigned untr = 0u;  // neighbours untrained at the window start
+      if (db <= 2 * kStage) {
+#if GS_OPT_HAB_B
 #pragma unroll
         for (int k = 0; k < kStage; ++k) {
-          const bool valid = k < dc, is_s = nb[k].x == s;
-          found |= valid && is_s;
-          age[k] = (valid && !is_s) ? S.eage[nb[k].y] : 0;
-          jv[k] = valid ? S.firstwin[nb[k].x] : kNone32;
+          if (k < db && S.hab[c1_nb0[k].x] >= P.h_t) untr |= 1u << k;
+          if (kStage + k < db && S.hab[c1_nb1[k].x] >= P.h_t) untr |= 1u << (kStage + k);
         }
-        int sv[kStage];
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          const bool risk = k < dc && nb[k].x != s && age[k] + 2 > P.max_age;
-          sv[k] = (risk && jv[k] < jj) ? rec[jv[k]].s : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          if (k >= dc) continue;
-          const bool age_risk = nb[k].x != s && age[k] + 2 > P.max_age;
-          if (!b_trained || age_risk) {
-            if (jv[k] < jj) kcn++;
-            if (age_risk) {
-              const int a2 = jv[k] < jj ? ((sv[k] == b) ? 0 : age[k] + 1) : age[k];
-              if (a2 + 1 > P.max_age) ev = true;
-            }
-          }
-        }
+#endif
+        b_chunk(S, P, rec, b, s, jj, b_trained, c1_nb0, min(kStage, db), c1_a0, c1_j0, acc);
+        b_chunk(S, P, rec, b, s, jj, b_trained, c1_nb1, db - kStage, c1_a1, c1_j1, acc);
+        c1_d = db;
+      } else {
+        ev = true;  // a winner of degree > 2 * kStage takes the serial path (rare)
       }
-      if (!found) ev = true;  // connect_or_reset creates b-s
-      const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, kcn), P.c_b) < P.h_t;
-      if (hb_low && w.dwin > thb) ev = true;  // maybe_insert fires
-      my_hblow = hb_low;
+      if (!acc.found) ev = true;  // connect_or_reset creates b-s
+      if (acc.ev) ev = true;
+      const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, acc.kcn), P.c_b) < P.h_t;
+      if (hb_low && my_dw > thb) ev = true;  // maybe_insert fires
       // last_active presence at the window start (dict order stamps)
       my_abs = (la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0);
       if (ev) evkey = ((long long)r << 32) | (unsigned)jj;
+#if !GS_OPT_HAB_B
+      if (!ev && !(ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) && hb_low) {
+#pragma unroll
+        for (int k = 0; k < kStage; ++k) {
+          if (k < db && S.hab[c1_nb0[k].x] >= P.h_t) untr |= 1u << k;
+          if (kStage + k < db && S.hab[c1_nb1[k].x] >= P.h_t) untr |= 1u << (kStage + k);
+        }
+      }
+#endif
+      if (!ev) c1_pat = adapt_outcome_staged(S, P, jj, hb_low, ringb, patb, db, c1_nb0, c1_nb1, untr);
+    }
+    // this thread's unit slot replayed as if the whole window commits
+    double4 wk_p;
+    double wk_h = 0.0, wk_h0 = 0.0;
+    int wk_max = -1;
+    if (g < nid_b) {
+      wk_h0 = S.hab[g];
+      wk_max = walk_compute(S, P, sig, g, wend, wk_p, wk_h);
     }
     // the first event: smallest rank, and its signal, in one cluster reduction
     const long long kmin = cl_min_ll(evkey, s_ll32, s_ctal, parity);
@@ -869,67 +975,49 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     const int rstar = has_ev ? (int)(kmin >> 32) : nproc;
     const int jstar = has_ev ? (int)(kmin & 0xffffffffLL) : wend;
     if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
-    // ---- C1: claims, last_active (+ order stamps), patience/threshold,
-    //      touched-unit owners, edge-age replay
+    // ---- C1: claims, last_active (+ order stamps), patience/threshold and
+    //      the edge ages each committed signal owns (the later toucher of an
+    //      edge replays it), stored from the values B computed
     const bool com = my_proc && my_rank >= rbase && my_rank < rstar;
-    WinRec cw;
-    int cj = 0;
+    int cb_com = -1;
     if (com) {
-      cj = my_j;
-      cw = rec[cj];
+      const int cj = my_j;
+      cb_com = cb;
       const long long ctick = tick0 + my_rank + 1;
       const int absent = my_abs;
-      S.claim[cw.b] = batch_no;
-      if (absent & 1) atomicMin(&S.la_stamp[cw.b], 3 * ctick);
-      if (absent & 2) atomicMin(&S.la_stamp[cw.s], 3 * ctick + 1);
-      atomicMax(&S.la_val[cw.b], ctick);
-      atomicMax(&S.la_val[cw.s], ctick);
-      const int p = adapt_outcome(S, P, cw.b, cj, my_hblow);
-      if (p != -2) {
-        S.patience[cw.b] = p & 0x3fffffff;
-        if (p >> 30) S.theta[cw.b] = dmul(S.theta[cw.b], P.rho);
+      S.claim[cb] = batch_no;
+      if (absent & 1) atomicMin(&S.la_stamp[cb], 3 * ctick);
+      if (absent & 2) atomicMin(&S.la_stamp[my_s], 3 * ctick + 1);
+      atomicMax(&S.la_val[cb], ctick);
+      atomicMax(&S.la_val[my_s], ctick);
+      if (c1_pat != -2) {
+        S.patience[cb] = c1_pat & 0x3fffffff;
+        if (c1_pat >> 30) S.theta[cb] = dmul(S.theta[cb], P.rho);
       }
-      const int db = S.deg[cw.b];
-      const int2* B = S.adj + (size_t)cw.b * kMaxDeg;
-      for (int c0 = 0; c0 < db; c0 += kStage) {
-        const int dc = min(kStage, db - c0);
-        int2 nb[kStage];
-        stage_adj(B + c0, dc, nb);
-        int jv[kStage], age[kStage];
 #pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          if (k < dc) {
-            jv[k] = S.firstwin[nb[k].x];
-            age[k] = S.eage[nb[k].y];
-          }
-        }
-        int sv[kStage];
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          const bool mine = k < dc && !(jv[k] < jstar && jv[k] > cj);
-          sv[k] = (mine && jv[k] < cj) ? rec[jv[k]].s : -1;
-        }
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          if (k >= dc) continue;
-          if (jv[k] < jstar && jv[k] > cj) continue;  // v's own signal replays this edge
-          int a = age[k];
-          if (jv[k] < cj) a = (sv[k] == cw.b) ? 0 : a + 1;
-          a = (nb[k].x == cw.s) ? 0 : a + 1;
-          S.eage[nb[k].y] = a;
-        }
+      for (int k = 0; k < kStage; ++k) {
+        // v's own committed signal (later than cj) replays the edge instead
+        if (k < c1_d && !(c1_j0[k] < jstar && c1_j0[k] > cj)) S.eage[c1_nb0[k].y] = c1_a0[k];
+        if (kStage + k < c1_d && !(c1_j1[k] < jstar && c1_j1[k] > cj))
+          S.eage[c1_nb1[k].y] = c1_a1[k];
       }
     }
-    csync();
-    if (lead) { const long long t_ = clock64(); acc[3] += t_ - t_ph; t_ph = t_; }
-    // ---- C2: each touched unit's position / habituation sequence replayed
-    //      once, over every unit slot: a unit no committed signal touched has
-    //      no replay key (its own and its neighbours' firstwin) and keeps its
-    //      values, so no touched list (nor the atomics to build one) is needed
-    const int nid = c->next_id;
-    for (int u = g; u < nid; u += kWinC) walk_unit(S, P, sig, u, jstar);
+    // ---- walk: each touched unit's position / habituation sequence in
+    //      batch order; the precomputed replay holds unless it used a signal
+    //      at or after the event (then this slot is replayed again)
+    const bool fast = !has_ev && nid_b <= kWinC;
+    if (wk_max >= 0) {
+      if (wk_max < jstar) walk_store(S, P, g, wk_p, wk_h, wk_h0);
+      else walk_unit(S, P, sig, g, jstar);
+    }
+    for (int u = g + kWinC; u < nid_b; u += kWinC) walk_unit(S, P, sig, u, jstar);
     const int deaths0 = c->deaths;  // stable until the event path
-    csync();
+    if (fast) {
+      // nothing reads firstwin after B here: clear the committed winners' now
+      if (com) S.firstwin[cb_com] = kNone32;
+    } else {
+      csync();  // the walks above read firstwin; clear after them
+    }
     if (lead) { const long long t_ = clock64(); acc[6] += t_ - t_ph; t_ph = t_; }
     // ---- counters, sweep clock, scratch reset
     // the window closes here unless an event without deaths lets it resume
@@ -943,7 +1031,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       while (ns <= tick0 + rstar) ns += kSweepEvery;
       c->next_sweep = ns;
     }
-    if (com) S.firstwin[cw.b] = kNone32;
+    if (!fast && com) S.firstwin[cb_com] = kNone32;
     // the event path reads neither firstwin nor the walked units' marks, and
     // its own barrier publishes these clears; only a next window that starts
     // right away needs them first
@@ -1103,6 +1191,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
     if (!resume) csync();  // firstwin cleared before the next window's candidates
   }
+  csync();  // the last window's walk stores are visible to the snapshot below
   {
     // row-ordered positions for the next find (its staging becomes coalesced
     // copies instead of a gather through rows), and the same rows as the

@@ -58,6 +58,12 @@ for lo, hi in zip(cuts, cuts[1:]):
     c = cyc[lo:hi].mean(axis=0)
     print(f"[{lo:5d},{hi:5d}) {1e3*r[lo:hi,1].mean():7.1f} {r[lo:hi,3].mean():6.1f} {r[lo:hi,4].mean():6.1f} "
           f"{c[0]:7.1f} " + " ".join(f"{c[1+q]:7.1f}" for q in PH))
+# serial-path causes per batch by slice (increments of the cumulative counters)
+evc = np.diff(np.concatenate([np.zeros((1, 4)), r[:, 7:11]]), axis=0)
+print("event causes per batch: events create insert prune sweep (an event may have several)")
+for lo, hi in zip(cuts, cuts[1:]):
+    c = evc[lo:hi].mean(axis=0)
+    print(f"[{lo:5d},{hi:5d}) {r[lo:hi, 3].mean():7.2f} " + " ".join(f"{x:7.2f}" for x in c))
 # update time vs events: least squares us = a + b*windows + c*events
 A = np.stack([np.ones(len(r)), r[:, 4], r[:, 3], r[:, 2]], 1)
 coef = np.linalg.lstsq(A, 1e3 * r[:, 1], rcond=None)[0]
