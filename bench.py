@@ -520,6 +520,45 @@ def find_microbench(lib, ctx, fp32_peak, peak_source, sizes=(10_000, 100_000, 1_
     return out
 
 
+def mesh_timing(net):
+    """SURVEY 8(f) row 3 at scale: mesh extraction + manifold check on the
+    device for a grown network (and the topology of a 1M-vertex torus grid),
+    beside the reference's host loops (metrics.py:148-240) on the same
+    network."""
+    import numpy as np
+
+    from paper_1503_08294_b200 import TriMesh, extract_mesh, manifold_check
+
+    extract_mesh(net)  # warm-up (allocator, module load)
+    t0 = time.perf_counter()
+    mesh = extract_mesh(net)
+    cls = manifold_check(mesh)
+    dev_s = time.perf_counter() - t0
+    n = 1000
+    i, j = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    a, b = i * n + j, i * n + (j + 1) % n
+    c, d = ((i + 1) % n) * n + j, ((i + 1) % n) * n + (j + 1) % n
+    grid = np.stack([np.stack([a, b, d], -1), np.stack([a, d, c], -1)], 2).reshape(-1, 3)
+    gmesh = TriMesh(np.zeros((n * n, 3)), grid.astype(np.int64))
+    manifold_check(gmesh)
+    t0 = time.perf_counter()
+    gcls = manifold_check(gmesh)
+    grid_s = time.perf_counter() - t0
+    out = {"units": int(net.unit_count), "faces": int(len(mesh.faces)), "manifold": cls,
+           "device_extract_and_check_s": dev_s,
+           "torus_grid_1M_vertices": {"faces": int(len(grid)), "manifold": gcls,
+                                      "device_check_s": grid_s}}
+    if reference_available():
+        import growsurf.metrics as rm
+
+        t0 = time.perf_counter()
+        rmesh = rm.extract_mesh(net)
+        rcls = rm.manifold_check(rmesh)
+        out["reference_host_s"] = time.perf_counter() - t0
+        out["same_faces"] = bool(np.array_equal(rmesh.faces, mesh.faces)) and rcls == cls
+    return out
+
+
 def fp32_peak(lib, ctx, sm_mhz, peaks):
     """(TFLOP/s, source): the FFMA2 probe measured on this GPU, else nominal."""
     t, ms = C.c_double(), C.c_double()
@@ -885,6 +924,7 @@ def run_b200_arm(args):
                           "host sampling of m, stats read each batch), max over ranks; "
                           "signals_per_s_wall adds the cloud H2D and setup",
                 "parallelism": f"signal-sharded find x{world}, replicated update"}
+        cfg4["mesh"] = mesh_timing(net4)
         net4.close()
         del src4
 

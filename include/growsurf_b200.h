@@ -51,6 +51,15 @@ typedef struct gs_ctx gs_ctx;
 
 gs_status gs_ctx_create(int device, gs_ctx **out);
 void gs_ctx_destroy(gs_ctx *ctx);
+/* Face-edge counts of a triangle list (metrics.py:165-240 _edge_face_counts /
+ * manifold_check / _is_connected / genus, on the device): faces n_faces x 3
+ * int64 (host) indexing [0, n_vertices); out[0] distinct face edges, out[1]
+ * edges bordering > 2 faces, out[2] boundary edges (1 face), out[3] vertices
+ * whose boundary degree is neither 0 nor 2, out[4] connected components of
+ * the face-edge graph over all n_vertices vertices, out[5] 0.
+ * GS_VALUE_ERROR for an index outside [0, n_vertices). */
+gs_status gs_mesh_topology(gs_ctx *ctx, const int64_t *faces, int64_t n_faces, int64_t n_vertices,
+                           int64_t out[6]);
 /* Number of SMs of the context's device (grid sizing, roofline). */
 int gs_ctx_sm_count(const gs_ctx *ctx);
 /* Measured FP32 peak of the device: packed FFMA2 chains on every SM, best of
@@ -263,6 +272,13 @@ gs_status gs_engine_set_run_state(gs_engine *eng, int64_t tick, int64_t next_swe
                                   const int64_t *stamp);
 /* All edges (a, b, age), a < b, sorted (network.py:152-161). */
 gs_status gs_engine_export_edges(gs_engine *eng, int64_t cap, int64_t *abage, int64_t *n_out);
+/* extract_mesh (metrics.py:148-163) on the device: every 3-clique a < b < c
+ * of the unit graph once, as indices of the id-ordered live units, in the
+ * reference's order.  *n_faces = the face count; faces (n x 3 int64) is
+ * written when cap >= it; topo (may be NULL) = gs_mesh_topology's counts of
+ * the same faces. */
+gs_status gs_engine_extract_mesh(gs_engine *eng, int64_t cap, int64_t *faces, int64_t *n_faces,
+                                 int64_t topo[6]);
 /* Device audit (Network.audit, network.py:485-526): recomputes rings, degree
  * symmetry, counters; returns the number of violations found. */
 gs_status gs_engine_audit(gs_engine *eng, int64_t *violations);

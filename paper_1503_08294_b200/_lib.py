@@ -104,6 +104,8 @@ _SIGNATURES = {
                                           C.c_int64, _vp, _vp, _vp, C.POINTER(C.c_int64)]),
     "gs_engine_set_run_state": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _vp, _vp, _vp]),
     "gs_engine_audit": (C.c_int, [_vp, C.POINTER(C.c_int64)]),
+    "gs_engine_extract_mesh": (C.c_int, [_vp, C.c_int64, _vp, C.POINTER(C.c_int64), _vp]),
+    "gs_mesh_topology": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, _vp]),
     "gs_sampler_create": (C.c_int, [_vp, _vp, C.c_int64, C.c_int, C.POINTER(_vp)]),
     "gs_sampler_destroy": (None, [_vp]),
     "gs_sampler_set_state": (C.c_int, [_vp, _u64p]),

@@ -254,6 +254,11 @@ __device__ __forceinline__ void best2_lex(Best2& b, double d, int32_t i) {
 }
 
 void find_launch(Ctx& ctx, const FindArgs& a, cudaStream_t stream, DevBuf& work);
+// face-list topology on the device (mesh.cu): out[6] = distinct face edges,
+// edges with > 2 faces, boundary edges, vertices with boundary degree not in
+// {0, 2}, connected components over the V vertices, bad-index flag
+void mesh_topology_device(Ctx& ctx, const int64_t* d_faces, int64_t F, int64_t V, int64_t out[6],
+                          cudaStream_t st);
 // sig[j] = pts[idx[j]] for j < m (sampled batches materialised for every rank)
 void gather_signals_launch(const int64_t* idx, const double* pts, double* sig, int64_t m,
                            cudaStream_t stream);

@@ -50,6 +50,7 @@
 #include <string>
 
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 #include <nccl.h>
 
 #include "common.cuh"
@@ -1648,6 +1649,136 @@ extern "C" gs_status gs_engine_step(gs_engine* e, const double* signals, int64_t
     harvest_timing(e);
     check_stats(e);
     if (out) *out = *e->h_stats;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// mesh extraction on the device (metrics.py:148-163 extract_mesh): every
+// 3-clique a < b < c of the unit graph once, as indices of the id-ordered
+// live units, in the reference's order (a ascending, then b, then c)
+
+namespace {
+__global__ void k_alive_flags(const uint8_t* __restrict__ alive, int n, int* __restrict__ flags) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
+    flags[u] = alive[u] ? 1 : 0;
+}
+
+// one thread per unit a: its neighbours above a, sorted; a face per pair
+// (b, c) of them that is an edge.  count pass: cnt[a]; write pass: faces
+// at off[a]
+__global__ void k_faces(DevState S, int n, const int* __restrict__ index,
+                        long long* __restrict__ cnt, const long long* __restrict__ off,
+                        int64_t* __restrict__ faces) {
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+    if (!S.alive[a]) {
+      if (!off) cnt[a] = 0;
+      continue;
+    }
+    const int d = S.deg[a];
+    const int2* A = S.adj + (size_t)a * kMaxDeg;
+    int up[kMaxDeg];
+    int k = 0;
+    for (int q = 0; q < d; ++q) {
+      const int v = A[q].x;
+      if (v > a) {
+        int i = k++;
+        while (i > 0 && up[i - 1] > v) {
+          up[i] = up[i - 1];
+          --i;
+        }
+        up[i] = v;
+      }
+    }
+    long long f = 0;
+    long long o = off ? off[a] : 0;
+    for (int i = 0; i < k; ++i) {
+      const int b = up[i];
+      const int db = S.deg[b];
+      const int2* B = S.adj + (size_t)b * kMaxDeg;
+      for (int j = i + 1; j < k; ++j) {
+        const int c = up[j];
+        bool hit = false;
+        for (int q = 0; q < db && !hit; ++q) hit = B[q].x == c;
+        if (hit) {
+          if (off) {
+            faces[3 * o] = index[a];
+            faces[3 * o + 1] = index[b];
+            faces[3 * o + 2] = index[c];
+            ++o;
+          }
+          ++f;
+        }
+      }
+    }
+    if (!off) cnt[a] = f;
+  }
+}
+}  // namespace
+
+extern "C" gs_status gs_engine_extract_mesh(gs_engine* e, int64_t cap, int64_t* faces,
+                                            int64_t* n_faces, int64_t topo[6]) {
+  return guarded([&] {
+    GS_CHECK(e && n_faces, GS_VALUE_ERROR, "null argument");
+    cudaStream_t st = e->stream;
+    Counters hc;
+    GS_CUDA(cudaMemcpyAsync(&hc, e->S.cnt, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    const int n = hc.next_id;
+    const int grid = 4 * e->ctx->sm_count, threads = 256;
+    size_t t1 = 0, t2 = 0;
+    GS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, (int*)nullptr, (int*)nullptr, n + 1, st));
+    GS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, (long long*)nullptr, (long long*)nullptr,
+                                          n + 1, st));
+    const size_t tb = std::max(t1, t2);
+    const size_t bi = ((sizeof(int) * (size_t)(n + 1)) + 255) & ~(size_t)255;
+    const size_t bl = ((sizeof(long long) * (size_t)(n + 1)) + 255) & ~(size_t)255;
+    char* base = (char*)dmalloc(2 * bi + 2 * bl + tb, st);
+    int* flags = (int*)base;
+    int* index = (int*)(base + bi);
+    long long* cnt = (long long*)(base + 2 * bi);
+    long long* off = (long long*)(base + 2 * bi + bl);
+    void* temp = base + 2 * bi + 2 * bl;
+    int64_t* d_faces = nullptr;
+    try {
+      GS_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(n + 1), st));
+      GS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(long long) * (size_t)(n + 1), st));
+      if (n) {
+        k_alive_flags<<<grid, threads, 0, st>>>(e->S.alive, n, flags);
+        k_faces<<<grid, threads, 0, st>>>(e->S, n, nullptr, cnt, nullptr, nullptr);
+        e->launches += 2;
+        g_launches += 2;
+      }
+      size_t ta = tb;
+      GS_CUDA(cub::DeviceScan::ExclusiveSum(temp, ta, flags, index, n + 1, st));
+      ta = tb;
+      GS_CUDA(cub::DeviceScan::ExclusiveSum(temp, ta, cnt, off, n + 1, st));
+      long long total = 0;
+      GS_CUDA(cudaMemcpyAsync(&total, off + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+      GS_CUDA(cudaStreamSynchronize(st));
+      *n_faces = total;
+      d_faces = (int64_t*)dmalloc(sizeof(int64_t) * 3 * (size_t)std::max<long long>(total, 1), st);
+      if (n && total) {
+        k_faces<<<grid, threads, 0, st>>>(e->S, n, index, cnt, off, d_faces);
+        e->launches++;
+        g_launches++;
+      }
+      GS_CUDA(cudaGetLastError());
+      if (topo) {
+        const unsigned long long before = g_launches;
+        mesh_topology_device(*e->ctx, d_faces, total, hc.n_units, topo, st);
+        e->launches += (long long)(g_launches - before);
+      }
+      if (faces && cap >= total && total)
+        GS_CUDA(cudaMemcpyAsync(faces, d_faces, sizeof(int64_t) * 3 * (size_t)total,
+                                cudaMemcpyDeviceToHost, st));
+      GS_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+      dfree(d_faces, st);
+      dfree(base, st);
+      throw;
+    }
+    dfree(d_faces, st);
+    dfree(base, st);
   });
 }
 
