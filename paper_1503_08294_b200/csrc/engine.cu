@@ -111,6 +111,7 @@ struct Counters {
   // (row 0 rounded to FP32) and max-norm of P' = fl32(p - centre), float bits
   double fcen[3];
   unsigned fpm_bits;
+  unsigned prof_bmax[2];  // GS_PROF_B builds: slowest B / walk chain of the window (cycles)
   int pad_;
 };
 
@@ -134,6 +135,7 @@ struct DevState {
   int32_t* claim;       // batch number that claimed the unit (multi.py:114-130)
   int32_t* firstwin;    // window scratch: first candidate signal per winner
   int32_t* touchfirst;  // window scratch: owner signal per touched unit
+  int32_t* ttr;         // window scratch: signal after which the unit is trained (walk)
   int32_t* iso_pos;     // index in iso_list or -1
   int32_t* rows;        // row -> id (append-only, id order)
   double* rowpos;       // [3][U] row-ordered positions (dead rows +inf) for the find
@@ -962,6 +964,7 @@ void grow_units(gs_engine* e, int new_u) {
   grow_array(S.claim, old, new_u, st);
   grow_array(S.firstwin, old, new_u, st);
   grow_array(S.touchfirst, old, new_u, st);
+  grow_array(S.ttr, old, new_u, st);
   grow_array(S.iso_pos, old, new_u, st);
   grow_array(S.rows, old, new_u, st);
   dfree(S.rowpos, st);  // regenerated by the next update (stride U)
@@ -983,6 +986,7 @@ void grow_units(gs_engine* e, int new_u) {
   GS_CUDA(cudaMemsetAsync(S.deg + old, 0, sizeof(int32_t) * add, st));
   fill_i32(S.firstwin + old, add, kNone32, st);
   fill_i32(S.touchfirst + old, add, kNone32, st);
+  fill_i32(S.ttr + old, add, -1, st);
   fill_i32(S.claim + old, add, -1, st);
   fill_i32(S.iso_pos + old, add, -1, st);
   fill_i64(S.la_val + old, add, -1, st);
@@ -1248,7 +1252,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   if (e->stream) cudaStreamSynchronize(e->stream);
   DevState& S = e->S;
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
-                  S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.iso_pos, S.rows, S.eage,
+                  S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.ttr, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
                   S.rowpos, S.rowf};
   for (void* q : ptrs) dfree(q, e->stream);  // stream is idle: back to the pool at once
@@ -1939,6 +1943,7 @@ extern "C" gs_status gs_engine_reset(gs_engine* e) {
     GS_CUDA(cudaMemsetAsync(S.deg, 0, sizeof(int32_t) * U, st));
     fill_i32(S.firstwin, U, kNone32, st);
     fill_i32(S.touchfirst, U, kNone32, st);
+    fill_i32(S.ttr, U, -1, st);
     fill_i32(S.claim, U, -1, st);
     fill_i32(S.iso_pos, U, -1, st);
     fill_i64(S.la_val, U, -1, st);

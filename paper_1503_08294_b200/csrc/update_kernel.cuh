@@ -28,6 +28,9 @@
 // Neighbour lists up to kStage long are staged in registers so their loads
 // (and the loads that depend on them) issue together instead of as a chain
 // of dependent L2 round trips; longer lists take the plain loops.
+#ifndef GS_PROF_B
+#define GS_PROF_B 0
+#endif
 #ifndef GS_STAGE
 #define GS_STAGE 8
 #endif
@@ -50,9 +53,6 @@ __device__ __forceinline__ void stage_adj(const int2* A, int d, int2 (&nb)[kStag
 #endif
 #ifndef GS_OPT_STAGEALL_W
 #define GS_OPT_STAGEALL_W 0
-#endif
-#ifndef GS_OPT_HAB_B
-#define GS_OPT_HAB_B 0
 #endif
 // the first kStage slots of a row regardless of the degree (rows hold kMaxDeg
 // slots, so the loads never leave the row): they issue together with the
@@ -85,14 +85,18 @@ __device__ __forceinline__ void replay_event(double4& p, double& h, const Params
 // so "smallest key above the last one" walks them in order without sorting.
 // Computes without storing: p / h are u's values after the replay, the
 // return value the largest signal index replayed (-1: none, u unchanged).
+// tt: the signal after whose update u's habituation first drops below h_t
+// (-1: trained already, kNone: not within the replay) -- habituation only
+// decays, so "u trained after the updates of signals <= j" is tt <= j.
 __device__ int walk_compute(const DevState& S, const Params& P, const double* sig, int u,
-                            int jstar, double4& p, double& h) {
+                            int jstar, double4& p, double& h, int& tt) {
   const int2* A = S.adj + (size_t)u * kMaxDeg;
   const int d = S.deg[u];
   const int jself = S.firstwin[u];
   p = S.pos[u];
   h = S.hab[u];
   constexpr int kNone = 0x7fffffff;
+  tt = h < P.h_t ? -1 : kNone;
   int last = -1;
   if (d <= 2 * kStage) {
     // up to 2*kStage neighbours: keys staged in registers, two chunks of loads
@@ -148,6 +152,7 @@ __device__ int walk_compute(const DevState& S, const Params& P, const double* si
           move_toward(p, P.eps_n, xs[q], ys[q], zs[q]);
           h = dmul(h, P.c_n);
         }
+        if (tt == kNone && h < P.h_t) tt = cur[q] >> 1;
       }
       if (cur[3] == kNone) break;
     }
@@ -161,6 +166,7 @@ __device__ int walk_compute(const DevState& S, const Params& P, const double* si
       }
       if (cur == kNone) break;
       replay_event(p, h, P, sig, cur);
+      if (tt == kNone && h < P.h_t) tt = cur >> 1;
       last = cur;
     }
   }
@@ -179,8 +185,9 @@ __device__ void walk_unit(const DevState& S, const Params& P, const double* sig,
                           int jstar) {
   double4 p;
   double h;
+  int tt;
   const double h0 = S.hab[u];
-  if (walk_compute(S, P, sig, u, jstar, p, h) >= 0) walk_store(S, P, u, p, h, h0);
+  if (walk_compute(S, P, sig, u, jstar, p, h, tt) >= 0) walk_store(S, P, u, p, h, h0);
 }
 
 // one chunk of the winner b's adjacency for B: the event tests (b-s edge
@@ -647,30 +654,54 @@ __device__ __noinline__ double hab_at(const DevState& S, const Params& P, int v,
   return pow_chain(hv, P.c_n, k2);
 }
 
-// adapt_threshold outcome (engine.py:208-265) of signal jj with winner b
-// (degree db <= 2 * kStage, adjacency staged in nb0 / nb1; bit k of untr:
-// neighbour k untrained at the window start), from the window-start state:
-// -2 none, else patience | shrink << 30
-__device__ __forceinline__ int adapt_outcome_staged(const DevState& S, const Params& P, int jj,
-                                                    bool hb_low, int ringb, int patb, int db,
-                                                    const int2 (&nb0)[kStage],
-                                                    const int2 (&nb1)[kStage], unsigned untr) {
-  if (ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) return 0;
-  if (!hb_low) return -2;
-  // every neighbour must be trained at time jj (engine.py:225-231); only the
-  // untrained-at-window-start ones need their decays replayed
-  bool ok = true;
+__device__ __forceinline__ bool adapt_ring_ok(const Params& P, int ringb) {
+  return ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf);
+}
+
+// neighbours past the walked slots (networks above kWinC units): trained at
+// time jj, from their decays replayed against the segment-start state (B)
+__device__ bool far_nbrs_trained(const DevState& S, const Params& P, int jj, int db,
+                                 const int2 (&nb0)[kStage], const int2 (&nb1)[kStage],
+                                 int nwalked) {
 #pragma unroll 1
-  for (; untr && ok; untr &= untr - 1) {
-    const int k = __ffs(untr) - 1;
+  for (int k = 0; k < db; ++k) {
     int v = -1;
 #pragma unroll
     for (int q = 0; q < kStage; ++q) {
       v = q == k ? nb0[q].x : v;
       v = kStage + q == k ? nb1[q].x : v;
     }
-    if (hab_at(S, P, v, S.hab[v], jj) >= P.h_t) ok = false;
+    if (v >= nwalked) {
+      const double hv = S.hab[v];
+      if (hv >= P.h_t && hab_at(S, P, v, hv, jj) >= P.h_t) return false;
+    }
   }
+  return true;
+}
+
+// adapt_threshold outcome (engine.py:208-265) of committed signal jj with
+// winner b (degree db <= 2 * kStage, adjacency staged in nb0 / nb1), from
+// the segment-start state: -2 none, else patience | shrink << 30.  Every
+// neighbour must be trained at time jj (engine.py:225-231): the walk of this
+// segment published each unit's time-to-trained (ttr, one load level for all
+// neighbours); neighbours past the walked slots were checked in B (far_ok).
+__device__ __forceinline__ int adapt_outcome_ttr(const DevState& S, const Params& P, int jj,
+                                                 bool hb_low, int ringb, int patb, int db,
+                                                 const int2 (&nb0)[kStage],
+                                                 const int2 (&nb1)[kStage], int nwalked,
+                                                 bool far_ok) {
+  if (adapt_ring_ok(P, ringb)) return 0;
+  if (!hb_low || !far_ok) return -2;
+  int t[2 * kStage];
+#pragma unroll
+  for (int k = 0; k < kStage; ++k) {
+    const int v0 = nb0[k].x, v1 = nb1[k].x;
+    t[k] = (k < db && v0 < nwalked) ? S.ttr[v0] : -1;
+    t[kStage + k] = (kStage + k < db && v1 < nwalked) ? S.ttr[v1] : -1;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 2 * kStage; ++k) ok &= t[k] <= jj;
   if (!ok) return -2;
   int cnt = patb + 1;
   const int shrink = cnt >= P.ring_patience ? 1 : 0;
@@ -893,12 +924,16 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     //      barrier between them is gone).
     const long long horizon = P.stale_factor * (long long)(n_units > 100 ? n_units : 100);
     long long evkey = 0x7fffffffffffffffLL;  // (rank << 32) | signal of this thread's event
-    int c1_pat = -2;                         // adapt_threshold outcome (adapt_outcome)
+    int c1_ring = 0, c1_patb = 0;            // adapt_threshold inputs (evaluated in C1)
+    bool c1_hblow = false, c1_far = true;
     int c1_d = 0;                            // winner degree (<= 2 * kStage)
     int2 c1_nb0[kStage], c1_nb1[kStage];     // its adjacency ...
     int c1_a0[kStage], c1_a1[kStage];        // ... edge ages after this signal ...
     int c1_j0[kStage], c1_j1[kStage];        // ... and the neighbours' first signals
     const int nid_b = c->next_id;
+#if GS_PROF_B
+    const long long tb0 = clock64();
+#endif
     if (my_proc && my_rank >= rbase) {
       const int r = my_rank;
       const int jj = my_j;
@@ -928,15 +963,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       const long long la_b = S.la_val[b], la_s = S.la_val[s];
       const bool b_trained = hbT < P.h_t;
       BScan acc{false, false, 0};
-      unsigned untr = 0u;  // neighbours untrained at the window start
       if (db <= 2 * kStage) {
-#if GS_OPT_HAB_B
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          if (k < db && S.hab[c1_nb0[k].x] >= P.h_t) untr |= 1u << k;
-          if (kStage + k < db && S.hab[c1_nb1[k].x] >= P.h_t) untr |= 1u << (kStage + k);
-        }
-#endif
         b_chunk(S, P, rec, b, s, jj, b_trained, c1_nb0, min(kStage, db), c1_a0, c1_j0, acc);
         b_chunk(S, P, rec, b, s, jj, b_trained, c1_nb1, db - kStage, c1_a1, c1_j1, acc);
         c1_d = db;
@@ -950,31 +977,52 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       // last_active presence at the window start (dict order stamps)
       my_abs = (la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0);
       if (ev) evkey = ((long long)r << 32) | (unsigned)jj;
-#if !GS_OPT_HAB_B
-      if (!ev && !(ringb == kRingDisk || (P.allow_boundary && ringb == kRingHalf)) && hb_low) {
-#pragma unroll
-        for (int k = 0; k < kStage; ++k) {
-          if (k < db && S.hab[c1_nb0[k].x] >= P.h_t) untr |= 1u << k;
-          if (kStage + k < db && S.hab[c1_nb1[k].x] >= P.h_t) untr |= 1u << (kStage + k);
-        }
-      }
-#endif
-      if (!ev) c1_pat = adapt_outcome_staged(S, P, jj, hb_low, ringb, patb, db, c1_nb0, c1_nb1, untr);
+      c1_ring = ringb;
+      c1_patb = patb;
+      c1_hblow = hb_low;
+      // the walk stores of C1's phase race with replays of units past the
+      // walked slots: those neighbours are checked here, against the
+      // segment-start state (networks above kWinC units only)
+      if (nid_b > kWinC && !ev && hb_low && !adapt_ring_ok(P, ringb))
+        c1_far = far_nbrs_trained(S, P, jj, db, c1_nb0, c1_nb1, kWinC);
     }
     // this thread's unit slot replayed as if the whole window commits
+#if GS_PROF_B
+    const long long tb1 = clock64();
+#endif
     double4 wk_p;
     double wk_h = 0.0, wk_h0 = 0.0;
     int wk_max = -1;
     if (g < nid_b) {
       wk_h0 = S.hab[g];
-      wk_max = walk_compute(S, P, sig, g, wend, wk_p, wk_h);
+      int tt;
+      wk_max = walk_compute(S, P, sig, g, wend, wk_p, wk_h, tt);
+      S.ttr[g] = tt;  // read by C1's adapt_threshold after the barrier below
     }
+#if GS_PROF_B
+    {  // the slowest thread's B and walk chains (cycles), cluster-wide max
+      const long long tb2 = clock64() + (wk_max & 0);  // after the walk's results
+      const unsigned db_ = __reduce_max_sync(0xffffffffu, (unsigned)min(tb1 - tb0, 0x7fffffffLL));
+      const unsigned dw_ = __reduce_max_sync(0xffffffffu, (unsigned)min(tb2 - tb1, 0x7fffffffLL));
+      if (lane == 0) {
+        atomicMax(&c->prof_bmax[0], db_);
+        atomicMax(&c->prof_bmax[1], dw_);
+      }
+    }
+#endif
     // the first event: smallest rank, and its signal, in one cluster reduction
     const long long kmin = cl_min_ll(evkey, s_ll32, s_ctal, parity);
     const bool has_ev = kmin != 0x7fffffffffffffffLL;
     const int rstar = has_ev ? (int)(kmin >> 32) : nproc;
     const int jstar = has_ev ? (int)(kmin & 0xffffffffLL) : wend;
     if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
+#if GS_PROF_B
+    if (lead) {
+      acc[3] += c->prof_bmax[0];
+      acc[10] += c->prof_bmax[1];
+      c->prof_bmax[0] = c->prof_bmax[1] = 0u;
+    }
+#endif
     // ---- C1: claims, last_active (+ order stamps), patience/threshold and
     //      the edge ages each committed signal owns (the later toucher of an
     //      edge replays it), stored from the values B computed
@@ -990,6 +1038,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (absent & 2) atomicMin(&S.la_stamp[my_s], 3 * ctick + 1);
       atomicMax(&S.la_val[cb], ctick);
       atomicMax(&S.la_val[my_s], ctick);
+      const int c1_pat = adapt_outcome_ttr(S, P, cj, c1_hblow, c1_ring, c1_patb, c1_d, c1_nb0,
+                                           c1_nb1, min(nid_b, kWinC), c1_far);
       if (c1_pat != -2) {
         S.patience[cb] = c1_pat & 0x3fffffff;
         if (c1_pat >> 30) S.theta[cb] = dmul(S.theta[cb], P.rho);

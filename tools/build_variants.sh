@@ -15,7 +15,8 @@ while [ $# -ge 2 ]; do
   name="$1"; defs="$2"; shift 2
   ( nvcc $FL $defs -c "$csrc/engine.cu" -o "$out/$name.engine.o" 2>/dev/null &&
     nvcc $ARCH -shared -o "$out/$name.so" "$csrc"/build/ctx.o "$csrc"/build/find.o \
-      "$csrc"/build/filter.o "$csrc"/build/grid.o "$csrc"/build/sample.o "$out/$name.engine.o" \
+      "$csrc"/build/filter.o "$csrc"/build/grid.o "$csrc"/build/sample.o "$csrc"/build/mesh.o \
+      "$out/$name.engine.o" \
       -lcudart -lnccl && rm -f "$out/$name.engine.o" && echo "built $name" ) &
   pids+=($!)
 done
