@@ -31,6 +31,12 @@
 #ifndef GS_PROF_B
 #define GS_PROF_B 0
 #endif
+#ifndef GS_PROF_TAIL
+#define GS_PROF_TAIL 0
+#endif
+#ifndef GS_STATS_FENCE
+#define GS_STATS_FENCE 0
+#endif
 #ifndef GS_STAGE
 #define GS_STAGE 8
 #endif
@@ -747,24 +753,33 @@ constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
 // used with alternating parity so a CTA running one call ahead cannot
 // overwrite values another CTA has not read yet.
-__device__ int cl_excl_scan(int v, int* s_warp, int (*s_cta)[kCluster], int& parity, int* total) {
+// free: optional (start, total) of the whole warps left over per CTA, i.e.
+// the exclusive scan of kUpdThreads - roundup32(CTA total) and its sum
+__device__ int cl_excl_scan(int v, int* s_warp, int (*s_cta)[kCluster], int& parity, int* total,
+                            int* blocal = nullptr, int* bcount = nullptr, int2* free = nullptr) {
   int btot;
   const int r = block_excl_scan(v, s_warp, &btot);
+  if (blocal) *blocal = r;
+  if (bcount) *bcount = btot;
   const int me = crank_of();
   if (threadIdx.x < kCluster) {
     int* dst = cmap(&s_cta[parity][0], threadIdx.x);
     dst[me] = btot;
   }
   csync();
-  int off = 0, tot = 0;
+  int off = 0, tot = 0, foff = 0, ftot = 0;
 #pragma unroll
   for (int q = 0; q < kCluster; ++q) {
     const int t = s_cta[parity][q];
+    const int f = kUpdThreads - ((t + 31) & ~31);
     off += q < me ? t : 0;
     tot += t;
+    foff += q < me ? f : 0;
+    ftot += f;
   }
   parity ^= 1;
   *total = tot;
+  if (free) *free = make_int2(foff, ftot);
   return off + r;
 }
 
@@ -821,6 +836,12 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
   __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
+  // this CTA's processed signals of the window, compacted in batch order:
+  // processed signal k of the CTA is evaluated (B, C1) by thread k, while
+  // the unit walks run on the CTA's top threads -- the two dependent-load
+  // chains of a window run on different warps instead of one after the other
+  __shared__ int4 s_pl[kUpdThreads];      // (signal, winner, second, rank)
+  __shared__ double s_pdw[kUpdThreads];   // d_winner
   Counters* c = S.cnt;
   const int tid = threadIdx.x;
   const int crank = crank_of();
@@ -867,11 +888,19 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   long long tick0 = 0, minla = 0;
   bool cand = false;
   int cb = -1;
-  int my_s = -1;      // this thread's record (second, d_winner): kept from A
+  int my_s = -1;      // this thread's window signal's record (second, d_winner)
   double my_dw = 0.0;
-  bool my_proc = false;  // this thread's window signal is processed ...
-  int my_rank = 0, my_j = 0;  // ... at this rank
-  int my_abs = 0;
+  bool my_proc = false;  // this thread's window signal is processed
+  // the processed signal this thread evaluates (CTA-local batch order)
+  bool p_valid = false;
+  int p_j = 0, p_b = -1, p_s = -1, p_rank = 0;
+  double p_dw = 0.0;
+  int p_abs = 0;
+  // the unit slot this thread walks (-1: none): the warps no processed
+  // signal occupies take the units, contiguous ranges per CTA from its last
+  // thread down; units past the free warps (nwalked) are walked after the
+  // window's reduction
+  int u_w = -1, nwalked = 0;
   while (j0 < m) {
     if (lead) t_ph = clock64();
     if (!resume) {
@@ -906,8 +935,28 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       // every thread keeps its own signal: its processing rank (batch
       // order among the processed signals) is all the later phases need
       my_proc = cand && S.firstwin[cb] == j;
-      my_rank = cl_excl_scan(my_proc ? 1 : 0, s_warp, s_cta, parity, &nproc);
-      my_j = j;
+      int bl, bcnt;
+      int2 fr;
+      const int my_rank =
+          cl_excl_scan(my_proc ? 1 : 0, s_warp, s_cta, parity, &nproc, &bl, &bcnt, &fr);
+      // whole warps: a warp that held both roles would run the two chains
+      // one after the other
+      u_w = tid >= ((bcnt + 31) & ~31) ? fr.x + (kUpdThreads - 1 - tid) : -1;
+      nwalked = fr.y;
+      if (my_proc) {
+        s_pl[bl] = make_int4(j, cb, my_s, my_rank);
+        s_pdw[bl] = my_dw;
+      }
+      __syncthreads();
+      p_valid = tid < bcnt;
+      if (p_valid) {
+        const int4 q = s_pl[tid];
+        p_j = q.x;
+        p_b = q.y;
+        p_s = q.z;
+        p_rank = q.w;
+        p_dw = s_pdw[tid];
+      }
       rbase = 0;
       if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
     }
@@ -934,10 +983,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #if GS_PROF_B
     const long long tb0 = clock64();
 #endif
-    if (my_proc && my_rank >= rbase) {
-      const int r = my_rank;
-      const int jj = my_j;
-      const int b = cb, s = my_s;
+    if (p_valid && p_rank >= rbase) {
+      const int r = p_rank;
+      const int jj = p_j;
+      const int b = p_b, s = p_s;
       const long long tick_j = tick0 + r + 1;
       bool ev = iso;
       if (tick_j >= next_sweep && ((tick_j - next_sweep) % kSweepEvery) == 0) {
@@ -973,9 +1022,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       if (!acc.found) ev = true;  // connect_or_reset creates b-s
       if (acc.ev) ev = true;
       const bool hb_low = b_trained || dmul(pow_chain(hbT, P.c_n, acc.kcn), P.c_b) < P.h_t;
-      if (hb_low && my_dw > thb) ev = true;  // maybe_insert fires
+      if (hb_low && p_dw > thb) ev = true;  // maybe_insert fires
       // last_active presence at the window start (dict order stamps)
-      my_abs = (la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0);
+      p_abs = (la_b == -1 ? 1 : 0) | (la_s == -1 ? 2 : 0);
       if (ev) evkey = ((long long)r << 32) | (unsigned)jj;
       c1_ring = ringb;
       c1_patb = patb;
@@ -983,32 +1032,35 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       // the walk stores of C1's phase race with replays of units past the
       // walked slots: those neighbours are checked here, against the
       // segment-start state (networks above kWinC units only)
-      if (nid_b > kWinC && !ev && hb_low && !adapt_ring_ok(P, ringb))
-        c1_far = far_nbrs_trained(S, P, jj, db, c1_nb0, c1_nb1, kWinC);
+      if (nid_b > nwalked && !ev && hb_low && !adapt_ring_ok(P, ringb))
+        c1_far = far_nbrs_trained(S, P, jj, db, c1_nb0, c1_nb1, nwalked);
     }
     // this thread's unit slot replayed as if the whole window commits
-#if GS_PROF_B
-    const long long tb1 = clock64();
-#endif
     double4 wk_p;
     double wk_h = 0.0, wk_h0 = 0.0;
     int wk_max = -1;
-    if (g < nid_b) {
-      wk_h0 = S.hab[g];
+    if (u_w >= 0 && u_w < nid_b) {
+      wk_h0 = S.hab[u_w];
       int tt;
-      wk_max = walk_compute(S, P, sig, g, wend, wk_p, wk_h, tt);
-      S.ttr[g] = tt;  // read by C1's adapt_threshold after the barrier below
+      wk_max = walk_compute(S, P, sig, u_w, wend, wk_p, wk_h, tt);
+      S.ttr[u_w] = tt;  // read by C1's adapt_threshold after the barrier below
     }
 #if GS_PROF_B
-    {  // the slowest thread's B and walk chains (cycles), cluster-wide max
-      const long long tb2 = clock64() + (wk_max & 0);  // after the walk's results
-      const unsigned db_ = __reduce_max_sync(0xffffffffu, (unsigned)min(tb1 - tb0, 0x7fffffffLL));
-      const unsigned dw_ = __reduce_max_sync(0xffffffffu, (unsigned)min(tb2 - tb1, 0x7fffffffLL));
-      if (lane == 0) {
-        atomicMax(&c->prof_bmax[0], db_);
-        atomicMax(&c->prof_bmax[1], dw_);
+    {  // the slowest thread's B / walk work before the reduction (cycles)
+      const long long tb2 = clock64() + (wk_max & 0) + (evkey & 0);
+      const unsigned db_ = __reduce_max_sync(0xffffffffu, (unsigned)min(tb2 - tb0, 0x7fffffffLL));
+      if (lane == 0) atomicMax(&c->prof_bmax[0], db_);
+      if (lead) acc[3] += tb2 - tb0;  // the lead's own work
+#ifdef GS_PROF_DUMP_BATCH
+      if (batch_no == GS_PROF_DUMP_BATCH && j0 == 0 && rbase == 0) {
+        const int du = u_w >= 0 && u_w < nid_b ? S.deg[u_w] : -1;
+        const int db = p_valid ? S.deg[p_b] : -1;
+        printf("D %d %d %lld %d %d %d %d %d\n", crank, tid, tb2 - tb0, p_valid ? 1 : 0, db,
+               u_w >= 0 && u_w < nid_b ? 1 : 0, du, wk_max >= 0 ? 1 : 0);
       }
+#endif
     }
+    const long long tb3 = clock64();
 #endif
     // the first event: smallest rank, and its signal, in one cluster reduction
     const long long kmin = cl_min_ll(evkey, s_ll32, s_ctal, parity);
@@ -1018,28 +1070,29 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
 #if GS_PROF_B
     if (lead) {
-      acc[3] += c->prof_bmax[0];
-      acc[10] += c->prof_bmax[1];
-      c->prof_bmax[0] = c->prof_bmax[1] = 0u;
+      acc[10] += c->prof_bmax[0];
+      acc[11] += clock64() - tb3;  // the reduction (block + cluster barrier)
+      c->prof_bmax[0] = 0u;
     }
 #endif
     // ---- C1: claims, last_active (+ order stamps), patience/threshold and
     //      the edge ages each committed signal owns (the later toucher of an
     //      edge replays it), stored from the values B computed
-    const bool com = my_proc && my_rank >= rbase && my_rank < rstar;
+    const bool com = p_valid && p_rank >= rbase && p_rank < rstar;
     int cb_com = -1;
     if (com) {
-      const int cj = my_j;
+      const int cj = p_j;
+      const int cb = p_b;
       cb_com = cb;
-      const long long ctick = tick0 + my_rank + 1;
-      const int absent = my_abs;
+      const long long ctick = tick0 + p_rank + 1;
+      const int absent = p_abs;
       S.claim[cb] = batch_no;
       if (absent & 1) atomicMin(&S.la_stamp[cb], 3 * ctick);
-      if (absent & 2) atomicMin(&S.la_stamp[my_s], 3 * ctick + 1);
+      if (absent & 2) atomicMin(&S.la_stamp[p_s], 3 * ctick + 1);
       atomicMax(&S.la_val[cb], ctick);
-      atomicMax(&S.la_val[my_s], ctick);
+      atomicMax(&S.la_val[p_s], ctick);
       const int c1_pat = adapt_outcome_ttr(S, P, cj, c1_hblow, c1_ring, c1_patb, c1_d, c1_nb0,
-                                           c1_nb1, min(nid_b, kWinC), c1_far);
+                                           c1_nb1, min(nid_b, nwalked), c1_far);
       if (c1_pat != -2) {
         S.patience[cb] = c1_pat & 0x3fffffff;
         if (c1_pat >> 30) S.theta[cb] = dmul(S.theta[cb], P.rho);
@@ -1055,12 +1108,12 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // ---- walk: each touched unit's position / habituation sequence in
     //      batch order; the precomputed replay holds unless it used a signal
     //      at or after the event (then this slot is replayed again)
-    const bool fast = !has_ev && nid_b <= kWinC;
+    const bool fast = !has_ev && nid_b <= nwalked;
     if (wk_max >= 0) {
-      if (wk_max < jstar) walk_store(S, P, g, wk_p, wk_h, wk_h0);
-      else walk_unit(S, P, sig, g, jstar);
+      if (wk_max < jstar) walk_store(S, P, u_w, wk_p, wk_h, wk_h0);
+      else walk_unit(S, P, sig, u_w, jstar);
     }
-    for (int u = g + kWinC; u < nid_b; u += kWinC) walk_unit(S, P, sig, u, jstar);
+    for (int u = nwalked + g; u < nid_b; u += kWinC) walk_unit(S, P, sig, u, jstar);
     const int deaths0 = c->deaths;  // stable until the event path
     if (fast) {
       // nothing reads firstwin after B here: clear the committed winners' now
@@ -1241,7 +1294,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
     if (!resume) csync();  // firstwin cleared before the next window's candidates
   }
+#if GS_PROF_TAIL
+  const long long tt0 = clock64();
+#endif
   csync();  // the last window's walk stores are visible to the snapshot below
+#if GS_PROF_TAIL
+  const long long tt1 = clock64();
+#endif
   {
     // row-ordered positions for the next find (its staging becomes coalesced
     // copies instead of a gather through rows), and the same rows as the
@@ -1304,6 +1363,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
     if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits, __float_as_uint(pm));
   }
+#if GS_PROF_TAIL
+  const long long tt2 = clock64();
+#endif
   if (crank != 0) return;
   if (tid == 0) c->rowpos_n = c->nrows;
   // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
@@ -1327,6 +1389,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
   }
   __syncthreads();
+#if GS_PROF_TAIL
+  if (tid == 0) {
+    const long long tt3 = clock64();
+    acc[3] += tt1 - tt0;   // tail: barrier
+    acc[10] += tt2 - tt1;  // tail: row snapshot
+    acc[11] += tt3 - tt2;  // tail: compaction check
+  }
+#endif
   if (tid == 0) {
     // is_converged: engine.py:358-365 (max(h) < h_t <=> no untrained unit)
     const int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
@@ -1362,7 +1432,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // the host's ring slot (pinned, mapped): no copy between the kernels
     if (st_out != st) {
       *st_out = *st;
-      __threadfence_system();
+#if GS_STATS_FENCE
+      __threadfence_system();  // (the host reads the slot only after an event)
+#endif
     }
   }
 }

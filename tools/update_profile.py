@@ -48,7 +48,9 @@ for d, part in enumerate(np.array_split(r, 10)):
     mu = part.mean(axis=0)
     print(f"{d:6d} {1e3*mu[0]:8.1f} {1e3*mu[1]:7.1f} {mu[2]:10.0f} {mu[3]:7.1f} {mu[4]:8.1f} {mu[5]:6.0f} {mu[6]:9.2f} "
           f"{mu[7]:9.2f} {mu[8]:9.2f} {mu[9]:8.2f} {mu[10]:8.2f}")
-PH = {0: "A+scan", 2: "B", 3: "Bwork", 10: "walkwork", 6: "walk", 7: "reset", 4: "ev:conn+mv", 5: "ev:ins+prune",
+# 3 / 10 / 11: profiling builds only (GS_PROF_B: slowest B / walk chain;
+# GS_PROF_TAIL: tail barrier / row snapshot / compaction check)
+PH = {0: "A+scan", 2: "B", 3: "x3", 10: "x10", 11: "x11", 6: "walk", 7: "reset", 4: "ev:conn+mv", 5: "ev:ins+prune",
       1: "ev:reclass", 8: "ev:adapt", 9: "ev:barrier"}
 cyc = np.diff(np.concatenate([np.zeros((1, 13)), r[:, 11:24]]), axis=0) / 1.9e3  # us at 1.9 GHz
 nb = len(r)
