@@ -204,6 +204,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// swizzled position of FP32 unit pair p (screened find staging, update
+// snapshot): within each row of 32 pairs the column is XORed with the row, so
+// a warp reading pairs l, l + 32, ... (one per lane) hits 32 distinct banks
+__host__ __device__ __forceinline__ int sf_swz(int p) {
+  return (p & ~31) | ((p ^ (p >> 5)) & 31);
+}
+
 // generic-proxy accesses of shared memory ordered before later async-proxy
 // (TMA) writes to it
 __device__ __forceinline__ void fence_proxy_async_smem() {

@@ -249,8 +249,6 @@ __global__ void __launch_bounds__(kSmallThreads) find_small_kernel(FindArgs a, i
 // non-finite or huge coordinates) or the list overflows (mass ties), the
 // warp scans every row exactly instead.
 
-constexpr int kSfThreads = 256;
-constexpr int kSfWarps = kSfThreads / 32;
 constexpr int kSfMaxRows = 4096;  // 16 B per row in shared memory
 constexpr int kSfCand = 128;      // candidate list per warp
 
@@ -296,25 +294,83 @@ __device__ __forceinline__ void sf_store_signals(const FindArgs& a, int64_t sig0
   }
 }
 
-template <int kFS>
-__global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, int tile_rows) {
-  extern __shared__ __align__(16) float4 s_u[];  // A0[npad] {ax0,ax1,ay0,ay1}, A1[npad] {az0,az1,w0,w1}
-  __shared__ float s_pm[kSfWarps];
-  __shared__ int32_t s_cand[kSfWarps][kSfCand];  // row * 4 + signal slot
-  __shared__ double s_d[kSfWarps][kSfCand];
-  __shared__ double s_q[kSfWarps][kFS][3];
+#ifdef GS_PROF_TL
+// timeline profiling builds: globaltimer stamps of every CTA for launches
+// [GS_PROF_TL - 100, GS_PROF_TL + 3), printed (tools/timeline.py parses them)
+__device__ unsigned g_sf_seq;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SF_TL(k) if (threadIdx.x == 0) tl[k] = gtimer()
+#else
+#define SF_TL(k)
+#endif
+
+// the screen's threshold T = e2 + 2 f + slack, every operation rounded up
+// (an upper bound of the same expression evaluated exactly; filter.cu's
+// error bound with a = Pmax, Q = |q - c|)
+__device__ __forceinline__ float sf_threshold(float e2, float pmaxf, double Qx, double Qy,
+                                              double Qz, bool& ok) {
+  const float ax = __double2float_ru(fabs(Qx)), ay = __double2float_ru(fabs(Qy)),
+              az = __double2float_ru(fabs(Qz));
+  const float q2 = __fmaf_ru(az, az, __fmaf_ru(ay, ay, __fmul_ru(ax, ax)));
+  ok = e2 < INFINITY && pmaxf * pmaxf <= 1e30f && q2 <= 1e30f;
+  const float u = 0x1p-24f, Q = __fsqrt_ru(q2), av = pmaxf;
+  const float dl = __fmaf_ru(u, av, __fmul_ru(__fmul_ru(u, 1.0f + 0x1p-23f), pmaxf));
+  float t = __fmul_ru(__fmul_ru(2.0f, dl), __fadd_ru(av, Q));
+  t = __fmaf_ru(dl, dl, t);
+  t = __fmaf_ru(__fmul_ru(6.02f * u, av), av, t);
+  t = __fmaf_ru(__fmul_ru(8.03f * u, av), Q, t);
+  const float fb = __fadd_ru(__fmul_ru(t, 1.0f + 1e-6f), 1e-38f);
+  const float slack = __fmul_ru(1e-14f, __fadd_ru(__fadd_ru(fabsf(e2), fb), q2));
+  return __fadd_ru(__fadd_ru(e2, __fmul_ru(2.0f, fb)), slack);
+}
+
+// kFS signals per warp, kW warps per CTA
+template <int kFS, int kW>
+__global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int tile_rows) {
+  static_assert(kFS == 1 || kFS == 2 || kFS == 4 || kFS == 8, "signals per warp");
+  // A0[npad] {ax0,ax1,ay0,ay1}, A1[npad] {az0,az1,w0,w1}, pair p at sf_swz(p)
+  extern __shared__ __align__(16) float4 s_u[];
+  __shared__ float s_pm[kW];
+  __shared__ int32_t s_cand[kW][kSfCand];  // (row << 3) | signal slot
+  __shared__ double s_d[kW][kSfCand];
+  __shared__ double s_q[kW][kFS][3];
+  __shared__ __align__(8) uint64_t s_bar;
+#ifdef GS_PROF_TL
+  unsigned long long tl[6] = {0, 0, 0, 0, 0, 0};
+  SF_TL(0);
+#endif
   const int npad = tile_rows / 2;  // unit pairs (tile_rows is a multiple of 128)
   float4* A0 = s_u;
   float4* A1 = s_u + npad;
+  const bool tma = a.rowpos && a.rowf;
+  if (threadIdx.x == 0 && tma) {
+    mbar_init(&s_bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
   // launched as a programmatic dependent of the previous kernel (the update):
   // every CTA may already be resident; wait for that grid's results here
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // ... and let the update (16 SMs) become resident on the SMs this grid
   // leaves free; it waits for this grid's records in turn
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  SF_TL(1);
+  // the update left the rows as swizzled FP32 unit pairs: two bulk copies of
+  // the whole tile (at most rowf_stride pairs) start before anything else;
+  // they are used only if that snapshot describes the current rows
+  const int ncopy = (int)(npad < a.rowf_stride ? (int64_t)npad : a.rowf_stride);
+  if (threadIdx.x == 0 && tma) {
+    mbar_expect_tx(&s_bar, 2u * 16u * (uint32_t)ncopy);
+    tma_bulk_g2s(A0, a.rowf, 16u * (uint32_t)ncopy, &s_bar);
+    tma_bulk_g2s(A1, a.rowf + a.rowf_stride, 16u * (uint32_t)ncopy, &s_bar);
+  }
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t sig0 = ((int64_t)blockIdx.x * kSfWarps + warp) * kFS;
+  const int64_t sig0 = ((int64_t)blockIdx.x * kW + warp) * kFS;
   const bool compact = a.rowpos && *a.rowpos_n == n;
 
   // signals (FP64, as the reference reads them)
@@ -337,24 +393,21 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
     }
   }
   bool full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
+  // the copies complete on the mbarrier whatever path follows
+  if (tma) mbar_wait(&s_bar, 0);
   if (!full_scan) {
     const int nr = (int)n;
     double cx = 0.0, cy = 0.0, cz = 0.0;
     float pm = 0.f;
-    if (compact && a.rowf) {
+    if (compact && tma) {
       // the update kernel left these rows as FP32 unit pairs (same centre
-      // rule, same bound): a coalesced copy
+      // rule, same bound, same swizzle): already staged
       cx = a.fcen[0];
       cy = a.fcen[1];
       cz = a.fcen[2];
       pm = __uint_as_float(*a.fpm_bits);
-      const int np64c = (((nr + 1) / 2) + 63) & ~63;
-      for (int p = threadIdx.x; p < np64c; p += kSfThreads) {
-        A0[p] = a.rowf[p];
-        A1[p] = a.rowf[a.rowf_stride + p];
-      }
-      __syncthreads();
     } else {
+      __syncthreads();  // every thread saw the copies land before they are overwritten
       // centre: row 0 rounded to FP32 (any centre is valid; the bound uses Pmax)
       if (nr > 0) {
         double x, y, z;
@@ -368,11 +421,11 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
       // thread per step with every load issued before any use (one memory
       // latency per step, not one per row).
       const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-      for (int p0 = threadIdx.x; p0 < npad; p0 += 4 * kSfThreads) {
+      for (int p0 = threadIdx.x; p0 < npad; p0 += 4 * 32 * kW) {
         double X[8], Y[8], Z[8];
   #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const int r = 2 * (p0 + (t >> 1) * kSfThreads) + (t & 1);
+          const int r = 2 * (p0 + (t >> 1) * 32 * kW) + (t & 1);
           X[t] = Y[t] = Z[t] = kInf;
           if (r < nr) {
             if (compact) {
@@ -386,7 +439,7 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         }
   #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int p = p0 + q * kSfThreads;
+          const int p = p0 + q * 32 * kW;
           if (p >= npad) break;
           float ax[2], ay[2], az[2], w[2];
   #pragma unroll
@@ -408,8 +461,8 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
               pm = (mn == mn) ? fmaxf(pm, mn) : INFINITY;  // NaN poisons Pmax
             }
           }
-          A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
-          A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+          A0[sf_swz(p)] = make_float4(ax[0], ax[1], ay[0], ay[1]);
+          A1[sf_swz(p)] = make_float4(az[0], az[1], w[0], w[1]);
         }
       }
   #pragma unroll
@@ -418,10 +471,11 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
       __syncthreads();
       pm = s_pm[0];
   #pragma unroll
-      for (int k = 1; k < kSfWarps; ++k) pm = fmaxf(pm, s_pm[k]);
+      for (int k = 1; k < kW; ++k) pm = fmaxf(pm, s_pm[k]);
     }
+    SF_TL(2);
     // |p - c| <= sqrt(3) * max_k |P'_k| / (1 - u), rounded up generously
-    const double pmax = (double)pm * 1.7320508075688774 * (1.0 + 1e-6);
+    const float pmaxf = __fmul_ru(pm, 1.7320508075688774f * (1.0f + 1e-6f));
 
     // pass 1: lane minima of e
     float2 fq[kFS][3];
@@ -438,8 +492,9 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
     const int np64 = (((nr + 1) / 2) + 63) & ~63;  // padded pairs are +inf
 #pragma unroll 1
     for (int p = lane; p < np64; p += 64) {
-      const float4 a0 = A0[p], a1 = A1[p];
-      const float4 c0 = A0[p + 32], c1 = A1[p + 32];
+      const int sa = sf_swz(p), sc = sf_swz(p + 32);
+      const float4 a0 = A0[sa], a1 = A1[sa];
+      const float4 c0 = A0[sc], c1 = A1[sc];
 #pragma unroll
       for (int k = 0; k < kFS; ++k) {
         float2 ea = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
@@ -451,8 +506,11 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         m1[k] = fminf(m1[k], fminf(fminf(ea.x, ea.y), fminf(ec.x, ec.y)));
       }
     }
-    // screen: thresholds, then the surviving lanes' units one by one
-    int cnt = 0;
+    SF_TL(3);
+    // screen: every signal's threshold (independent chains, issued together),
+    // then the surviving lanes' units one by one
+    float T[kFS];
+    unsigned tasks[kFS];
 #pragma unroll
     for (int k = 0; k < kFS; ++k) {
       float v1 = m1[k], v2 = INFINITY;  // two smallest lane minima
@@ -463,52 +521,51 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         v2 = fminf(fmaxf(v1, o1), fminf(v2, o2));
         v1 = fminf(v1, o1);
       }
-      const double Qx = qx[k] - cx, Qy = qy[k] - cy, Qz = qz[k] - cz;
-      const double q2 = Qx * Qx + Qy * Qy + Qz * Qz;
-      if (!(v2 < INFINITY && pmax * pmax <= 1e30 && q2 <= 1e30)) {
-        full_scan = true;  // warp-uniform
-        continue;
-      }
-      const double u = 0x1p-24, Q = sqrt(q2), av = pmax;
-      const double dl = u * (1.0 + u) * pmax + u * av;
-      const double f =
-          (2.0 * dl * (av + Q) + dl * dl + 6.02 * u * av * av + 8.03 * u * av * Q) * (1.0 + 1e-6) +
-          1e-44;
-      const double e2 = (double)v2;
-      const float T = __double2float_ru(e2 + 2.0 * f + 1e-14 * (fabs(e2) + f + q2));
-      unsigned tasks = __ballot_sync(0xffffffffu, m1[k] <= T);
-      while (tasks) {
-        const int l = __ffs(tasks) - 1;
-        tasks &= tasks - 1;
-        for (int i0 = 0; i0 < np64 / 32; i0 += 32) {  // lane l's pairs l + 32 i, one per lane
-          const int p = 32 * (i0 + lane) + l;
-          const bool in = p < np64;
-          const float4 a0 = in ? A0[p] : make_float4(0.f, 0.f, 0.f, 0.f);
-          const float4 a1 = in ? A1[p] : make_float4(0.f, 0.f, INFINITY, INFINITY);
-          float2 e = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
-          e = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], e);
-          e = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], e);
+      bool ok;
+      T[k] = sf_threshold(v2, pmaxf, qx[k] - cx, qy[k] - cy, qz[k] - cz, ok);
+      full_scan |= !ok;  // warp-uniform
+      tasks[k] = __ballot_sync(0xffffffffu, m1[k] <= T[k]);
+    }
+    int cnt = 0;
+    if (!full_scan) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const bool pass = in && (h ? e.y : e.x) <= T;
-            const unsigned bal = __ballot_sync(0xffffffffu, pass);
-            const int at = cnt + __popc(bal & ((1u << lane) - 1u));
-            if (pass && at < kSfCand) s_cand[warp][at] = (2 * p + h) * 4 + k;
-            cnt += __popc(bal);
+      for (int k = 0; k < kFS; ++k) {
+        unsigned tk = tasks[k];
+        while (tk) {
+          const int l = __ffs(tk) - 1;
+          tk &= tk - 1;
+          for (int i0 = 0; i0 < np64 / 32; i0 += 32) {  // lane l's pairs l + 32 i, one per lane
+            const int p = 32 * (i0 + lane) + l;
+            const bool in = p < np64;
+            const int sp = sf_swz(p);  // conflict-free: lane i reads row i, column l ^ i
+            const float4 a0 = in ? A0[sp] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 a1 = in ? A1[sp] : make_float4(0.f, 0.f, INFINITY, INFINITY);
+            float2 e = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
+            e = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], e);
+            e = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], e);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const bool pass = in && (h ? e.y : e.x) <= T[k];
+              const unsigned bal = __ballot_sync(0xffffffffu, pass);
+              const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+              if (pass && at < kSfCand) s_cand[warp][at] = ((2 * p + h) << 3) | k;
+              cnt += __popc(bal);
+            }
           }
         }
-      }
-      if (lane == 0) {
-        s_q[warp][k][0] = qx[k];
-        s_q[warp][k][1] = qy[k];
-        s_q[warp][k][2] = qz[k];
+        if (lane == 0) {
+          s_q[warp][k][0] = qx[k];
+          s_q[warp][k][1] = qy[k];
+          s_q[warp][k][2] = qz[k];
+        }
       }
     }
     if (!full_scan && cnt <= kSfCand) {
       __syncwarp();
+      SF_TL(4);
       for (int c = lane; c < cnt; c += 32) {  // exact FP64 distance per candidate
         const int code = s_cand[warp][c];
-        const int r = code >> 2, k = code & 3;
+        const int r = code >> 3, k = code & 7;
         double x, y, z;
         double d = __longlong_as_double(0x7ff8000000000000LL);  // NaN: never selected
         if (sf_row(a, compact, r, x, y, z))
@@ -521,12 +578,25 @@ __global__ void __launch_bounds__(kSfThreads) find_small_f32_kernel(FindArgs a, 
         b.init();
         for (int c = 0; c < cnt; ++c) {
           const int code = s_cand[warp][c];
-          if ((code & 3) == lane) best2_lex(b, s_d[warp][c], code >> 2);
+          if ((code & 7) == lane) best2_lex(b, s_d[warp][c], code >> 3);
         }
         const int64_t j = sig0 + lane;
         if (j < a.m) write_result(a, j, b);
       }
       sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
+#ifdef GS_PROF_TL
+      SF_TL(5);
+      __shared__ unsigned s_seq;
+      if (threadIdx.x == 0) s_seq = *(volatile unsigned*)&g_sf_seq;
+      __syncthreads();
+      if (threadIdx.x == 0 && s_seq + 100 >= GS_PROF_TL && s_seq < GS_PROF_TL + 3) {
+        unsigned smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("F %u %u %u %llu %llu %llu %llu %llu %llu\n", s_seq, blockIdx.x, smid, tl[0],
+               tl[1], tl[2], tl[3], tl[4], tl[5]);
+      }
+      if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_sf_seq, 1u);
+#endif
       return;
     }
     full_scan = true;
@@ -599,41 +669,36 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
       find_filter_launch(ctx, a, stream, work))
     return;
   if (a.mode != GS_FIND_EXACT && a.n <= kSfMaxRows) {
-    static bool sf_attr = false;
-    if (!sf_attr) {
-      const int bytes = 16 * kSfMaxRows;
-      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      GS_CUDA(cudaFuncSetAttribute(find_small_f32_kernel<4>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      sf_attr = true;
-    }
-    // rows staged: the estimate plus headroom for growth in flight, a
-    // multiple of 128 (whole 64-pair steps)
-    const int tile_rows = (int)std::min<int64_t>(
-        kSfMaxRows, ((std::max<int64_t>(a.n, 1) + 512 + 127) / 128) * 128);
-    const size_t smem = 16 * (size_t)tile_rows;
-    const int64_t warps = kSfThreads / 32;
-    // signals per warp: the most that still gives most SMs two CTAs (the
-    // second hides the first one's staging latency; measured on cfg3)
+    // signals per warp and warps per CTA: enough CTAs for every SM, each
+    // staged row pair feeding as many signals as that allows (pass 1 is
+    // bound by shared-memory wavefronts: 8 signals per load at cfg3's m)
     static int fs_env = -1;
     if (fs_env < 0) {
       const char* e = getenv("GS_SF_FS");
       fs_env = e ? atoi(e) : 0;
     }
-    int fs = fs_env;
-    if (fs != 1 && fs != 2 && fs != 4) {
-      const int64_t sms = ctx.sm_count;
-      fs = (a.m * 100 >= 170 * warps * 4 * sms) ? 4 : (a.m * 100 >= 170 * warps * 2 * sms) ? 2 : 1;
+    const int64_t sms = ctx.sm_count;
+    int fs = fs_env, w = 8;
+    if (fs != 1 && fs != 2 && fs != 4 && fs != 8) {
+      // the most signals per warp that still gives most SMs two 8-warp CTAs
+      // (the second hides the first one's staging; measured on cfg3: 2 at
+      // m = 4096 beats 4 and 8)
+      fs = 1;
+      for (int c : {8, 4, 2})
+        if (a.m * 100 >= (int64_t)170 * 8 * c * sms) { fs = c; break; }
     }
-    const unsigned grid = (unsigned)((a.m + warps * fs - 1) / (warps * fs));
+    if (fs >= 4) w = 4;
+    // rows staged: the estimate plus headroom for growth in flight, a
+    // multiple of 128 (whole 64-pair steps)
+    const int tile_rows = (int)std::min<int64_t>(
+        kSfMaxRows, ((std::max<int64_t>(a.n, 1) + 512 + 127) / 128) * 128);
+    const size_t smem = 16 * (size_t)tile_rows;
+    const unsigned grid = (unsigned)((a.m + w * fs - 1) / (w * fs));  // a warp owns fs signals
     // programmatic dependent launch: the CTAs become resident while the
     // previous kernel (the 16-SM update) still runs and wait in-kernel
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kSfThreads);
+    cfg.blockDim = dim3(32 * w);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -641,12 +706,24 @@ void find_launch(Ctx& ctx, const FindArgs& a_in, cudaStream_t stream, DevBuf& wo
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (fs == 4)
-      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<4>, a, tile_rows));
-    else if (fs == 2)
-      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<2>, a, tile_rows));
-    else
-      GS_CUDA(cudaLaunchKernelEx(&cfg, find_small_f32_kernel<1>, a, tile_rows));
+    static bool sf_attr = false;
+    if (!sf_attr) {
+      for (auto kern : {find_small_f32_kernel<8, 4>, find_small_f32_kernel<4, 4>,
+                        find_small_f32_kernel<2, 8>, find_small_f32_kernel<2, 4>,
+                        find_small_f32_kernel<1, 8>, find_small_f32_kernel<1, 4>})
+        GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     16 * kSfMaxRows));
+      sf_attr = true;
+    }
+    auto go = [&](void (*kern)(FindArgs, int)) {
+      GS_CUDA(cudaLaunchKernelEx(&cfg, kern, a, tile_rows));
+    };
+    if (fs == 8) go(find_small_f32_kernel<8, 4>);
+    else if (fs == 4) go(find_small_f32_kernel<4, 4>);
+    else if (fs == 2 && w == 8) go(find_small_f32_kernel<2, 8>);
+    else if (fs == 2) go(find_small_f32_kernel<2, 4>);
+    else if (w == 8) go(find_small_f32_kernel<1, 8>);
+    else go(find_small_f32_kernel<1, 4>);
     GS_CUDA(cudaGetLastError());
     ++g_launches;
     return;

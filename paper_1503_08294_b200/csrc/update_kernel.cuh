@@ -849,9 +849,16 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const bool lead = crank == 0 && tid == 0;
   const int warp = tid >> 5, lane = tid & 31;
   int parity = 0;
+#ifdef GS_PROF_TL
+  unsigned long long tl0, tl1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl0));
+#endif
   // programmatic dependent launch after the find: wait for its records
   // here; the next batch's find may launch at once (its CTAs wait in turn)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef GS_PROF_TL
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl1));
+#endif
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (S.cnt->halted) {  // converged earlier in an asynchronous run (uniform)
     // the batch's stats slot still gets the (unchanged) latest values
@@ -1356,8 +1363,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           }
         }
       }
-      A0[p] = make_float4(ax[0], ax[1], ay[0], ay[1]);
-      A1[p] = make_float4(az[0], az[1], w[0], w[1]);
+      A0[sf_swz(p)] = make_float4(ax[0], ax[1], ay[0], ay[1]);  // the find's swizzle
+      A1[sf_swz(p)] = make_float4(az[0], az[1], w[0], w[1]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
@@ -1429,6 +1436,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     st->batches = c->batches;
     st->halted = c->halted;
     for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
+#ifdef GS_PROF_TL
+    if (batch_no >= GS_PROF_TL && batch_no < GS_PROF_TL + 3) {
+      unsigned long long tl2;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      printf("U %d %u %llu %llu %llu %lld\n", batch_no, smid, tl0, tl1, tl2, c->windows);
+    }
+#endif
     // the host's ring slot (pinned, mapped): no copy between the kernels
     if (st_out != st) {
       *st_out = *st;
