@@ -254,6 +254,7 @@ struct FindArgs {
   double* out_d2 = nullptr;
   WinRec* out_win = nullptr;
   int mode = GS_FIND_AUTO;
+  int tl_batch = -1;             // timeline profiling builds: the update batch this feeds
 };
 
 // row r of a find's unit set (false: a dead engine slot)

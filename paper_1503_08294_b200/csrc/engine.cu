@@ -70,6 +70,7 @@ constexpr int kUpdThreads = GS_UPD_THREADS;
 constexpr long long kSweepEvery = 1024;  // engine.py:98
 constexpr int kAffCap = kMaxDeg * (kMaxDeg + 2) + 64;
 constexpr int kDeferCap = 16384;
+constexpr int kDeferSm = 512;  // deferred ring recomputes held in shared memory (event path)
 
 enum DevError {
   E_NONE = 0,
@@ -147,6 +148,7 @@ struct DevState {
   int32_t* aff;         // [kAffCap] ring-recompute set
   int32_t* defer_list;  // [kDeferCap] deferred ring recomputes (event path)
   int* defer_n;         // non-null: recompute_ring defers (set per launch)
+  int* defer_sm;        // the event path's shared-memory part of the deferred list
   Counters* cnt;
   gs_batch_stats* stats;
   int U, EC;
@@ -242,18 +244,26 @@ __device__ int classify_ring(const DevState& S, int u) {
   return __popcll(seen) == k ? shape : kRingInc;
 }
 
+// deferred ring recompute (event path): the first kDeferSm entries in shared
+// memory, the rest in S.defer_list; duplicates are dropped when the list is
+// consumed (a ring is a pure function of the final adjacency)
+__device__ __forceinline__ void defer_push(const DevState& S, int u) {
+  const int k = atomicAdd(S.defer_n, 1);
+  if (k < kDeferSm) S.defer_sm[k] = u;
+  else if (k < kDeferSm + kDeferCap) S.defer_list[k - kDeferSm] = u;
+  else set_err(S, E_AFF);
+}
+__device__ __forceinline__ int defer_at(const DevState& S, const int* sm, int k) {
+  return k < kDeferSm ? sm[k] : S.defer_list[k - kDeferSm];
+}
+
 // _recompute_ring: network.py:416-422
 __device__ void recompute_ring(const DevState& S, int u) {
   if (S.defer_n) {
     // batch-kernel event path: rings are a pure function of the final
     // adjacency and only read after the topology changes, so collect the
-    // affected units (once each) and reclassify them in parallel afterwards
-    if (S.touchfirst[u] != -2) {
-      S.touchfirst[u] = -2;
-      const int k = (*S.defer_n)++;
-      if (k < kDeferCap) S.defer_list[k] = u;
-      else set_err(S, E_AFF);
-    }
+    // affected units and reclassify them in parallel afterwards
+    defer_push(S, u);
     return;
   }
   const int nw = classify_ring(S, u);
@@ -697,6 +707,14 @@ __device__ int block_sum(int v, int* s_warp) {
   return total;
 }
 
+#ifdef GS_PROF_TL
+// timeline profiling builds: per batch, the update's lead thread stamps
+// (resident, wait released, end) in globaltimer ns
+__device__ unsigned long long g_tlu[8192][3];
+extern "C" int gs_debug_tl_update(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_tlu, sizeof(unsigned long long) * 3 * (size_t)n);
+}
+#endif
 #include "update_kernel.cuh"
 
 // ---------------------------------------------------------------------------
@@ -1161,6 +1179,7 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   a.m = hi - lo;
   a.out_win = d_rec + lo;
   a.mode = e->hp.find_mode;
+  a.tl_batch = e->batch_no + 1;  // the update this find feeds (timeline builds)
   const unsigned long long before = g_launches;
   find_launch(*e->ctx, a, e->stream, e->find_work);
   e->launches += (long long)(g_launches - before);

@@ -304,6 +304,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 #define SF_TL(k) if (threadIdx.x == 0) tl[k] = gtimer()
+// per batch: wait released (CTA 0), last CTA's end, CTA count
+__device__ unsigned long long g_tlf[8192][3];
+extern "C" int gs_debug_tl_find(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_tlf, sizeof(unsigned long long) * 3 * (size_t)n);
+}
 #else
 #define SF_TL(k)
 #endif
@@ -586,10 +591,16 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
       sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
 #ifdef GS_PROF_TL
       SF_TL(5);
+      if (threadIdx.x == 0 && a.tl_batch >= 0) {
+        unsigned long long* g = g_tlf[a.tl_batch & 8191];
+        if (blockIdx.x == 0) g[0] = tl[1];
+        atomicMax(&g[1], tl[5]);
+        atomicAdd(&g[2], 1ull);
+      }
       __shared__ unsigned s_seq;
       if (threadIdx.x == 0) s_seq = *(volatile unsigned*)&g_sf_seq;
       __syncthreads();
-      if (threadIdx.x == 0 && s_seq + 100 >= GS_PROF_TL && s_seq < GS_PROF_TL + 3) {
+      if (threadIdx.x == 0 && s_seq + 100 >= GS_PROF_TL && s_seq < GS_PROF_TL + 3 && GS_PROF_TL > 0) {
         unsigned smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
         printf("F %u %u %u %llu %llu %llu %llu %llu %llu\n", s_seq, blockIdx.x, smid, tl[0],

@@ -34,6 +34,9 @@
 #ifndef GS_PROF_TAIL
 #define GS_PROF_TAIL 0
 #endif
+#ifndef GS_PROF_EV
+#define GS_PROF_EV 0
+#endif
 #ifndef GS_STATS_FENCE
 #define GS_STATS_FENCE 0
 #endif
@@ -394,15 +397,9 @@ __device__ int w_find_slot(const DevState& S, int a, int b) {
   return -1;
 }
 
-// deferred _recompute_ring for u (each unit queued once; lanes may call it
-// concurrently for different units)
-__device__ __forceinline__ void w_defer(const DevState& S, int u) {
-  if (atomicExch(&S.touchfirst[u], -2) != -2) {
-    const int k = atomicAdd(S.defer_n, 1);
-    if (k < kDeferCap) S.defer_list[k] = u;
-    else set_err(S, E_AFF);
-  }
-}
+// deferred _recompute_ring for u (lanes may call it concurrently; the list
+// is deduplicated when it is consumed)
+__device__ __forceinline__ void w_defer(const DevState& S, int u) { defer_push(S, u); }
 
 // defer the rings of _ring_neighborhood(a, b) (network.py:424-433): the
 // common neighbours of a and b, then a and b.  stage: per-warp smem (64 ints)
@@ -592,18 +589,19 @@ __device__ void w_event_part1a(const DevState& S, const Params& P, int b, int s,
 
 // maybe_insert + prune (engine.py:335-344), whole warp; 1 when the sweep
 // clock fired (uniform)
+// (thb, hb, wp: the winner's threshold, habituation and position after its
+// move, as the first part left them)
 __device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, double dw,
                               double x, double y, double z, const int* over, int nover,
-                              int* stage) {
+                              int* stage, double thb, double hb, const double4& wp) {
   const int lane = threadIdx.x & 31;
   Counters* c = S.cnt;
   const long long tick = c->tick;
-  if (dw > S.theta[b] && S.hab[b] < P.h_t) {
+  if (dw > thb && hb < P.h_t) {
     int r = -1;
     if (lane == 0) {
-      const double4 wp = S.pos[b];
       r = add_unit(S, P, dmul(dadd(wp.x, x), 0.5), dmul(dadd(wp.y, y), 0.5),
-                   dmul(dadd(wp.z, z), 0.5), S.theta[b]);
+                   dmul(dadd(wp.z, z), 0.5), thb);
     }
     r = __shfl_sync(0xffffffffu, r, 0);
     __syncwarp();
@@ -628,6 +626,142 @@ __device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, 
     fired = tick >= c->next_sweep ? 1 : 0;
   }
   return __shfl_sync(0xffffffffu, fired, 0);
+}
+
+// update_single up to and including the moves (engine.py:297-333) for a
+// winner and second of degree < 32, with every load issued up front: the two
+// rows, the winner's / second's scalars and the top of the free-edge stack in
+// one level, the winner's edge ages and neighbours' positions in the next;
+// then connect_or_reset (network.py:261-282), the ring-neighbourhood defers
+// (common neighbours from the two staged rows), age_incident_edges
+// (network.py:294-319, over-age neighbours in row order) and the moves run on
+// registers.  Whole warp, uniform arguments; lane 0's thb / hb / pb: the
+// winner's threshold, habituation and position afterwards.
+__device__ void w_event_first(const DevState& S, const Params& P, int b, int s, double x,
+                              double y, double z, int db, int2 eb, int ds, int2 es, int* over,
+                              int* nover, int* stage, double& thb, double& hb, double4& pb) {
+  const int lane = threadIdx.x & 31;
+  Counters* c = S.cnt;
+  // level 2 loads (the rows came with the caller's dispatch)
+  long long la = 0;
+  if (lane < 2) la = S.la_val[lane ? s : b];
+  double4 ps = make_double4(0.0, 0.0, 0.0, 0.0);
+  double hs = 0.0;
+  int enext = -1;
+  const int top = c->efree_top;
+  if (lane == 0) {
+    pb = S.pos[b];
+    hb = S.hab[b];
+    thb = S.theta[b];
+    ps = S.pos[s];
+    hs = S.hab[s];
+    if (top > 0) enext = S.efree[top - 1];
+  }
+  // level 3: the winner's edge ages and neighbours
+  int ag = 0;
+  double4 pv = make_double4(0.0, 0.0, 0.0, 0.0);
+  double hv = 0.0;
+  if (lane < db) {
+    ag = S.eage[eb.y];
+    pv = S.pos[eb.x];
+    hv = S.hab[eb.x];
+  }
+  // touch_active(b), touch_active(s) (engine.py:301-302): distinct units
+  long long tick = 0;
+  if (lane == 0) tick = ++c->tick;
+  tick = __shfl_sync(0xffffffffu, tick, 0);
+  if (lane < 2) {
+    const int u = lane ? s : b;
+    if (la == -1) S.la_stamp[u] = 3 * tick + lane;
+    S.la_val[u] = tick;
+  }
+  // connect_or_reset(b, s)
+  const unsigned fb = __ballot_sync(0xffffffffu, lane < db && eb.x == s);
+  int created;
+  if (fb) {
+    const int k = __ffs(fb) - 1;
+    if (lane == k) S.eage[eb.y] = 0;
+    created = 0;
+  } else {
+    int ok = 0;
+    if (lane == 0) {
+      if (top <= 0) {
+        set_err(S, E_EDGE_CAP);
+      } else {
+        c->efree_top = top - 1;
+        const int e = enext;
+        S.eage[e] = 0;
+        if (db == 0) iso_del(S, b);
+        if (ds == 0) iso_del(S, s);
+        S.adj[(size_t)b * kMaxDeg + db] = make_int2(s, e);
+        S.adj[(size_t)s * kMaxDeg + ds] = make_int2(b, e);
+        S.deg[b] = db + 1;
+        S.deg[s] = ds + 1;
+        c->n_edges++;
+        const int dm = max(db, ds) + 1;
+        if (dm > c->max_degree) c->max_degree = dm;
+        c->ev_create++;
+        ok = 1;
+      }
+    }
+    ok = __shfl_sync(0xffffffffu, ok, 0);
+    created = ok ? 1 : -1;
+    if (ok) {
+      // _ring_neighborhood(b, s) (network.py:424-433): the common neighbours
+      // of the rows before the new edge, then b and s
+      if (lane < ds) stage[lane] = es.x;
+      __syncwarp();
+      bool common = false;
+      if (lane < db && eb.x != s)
+        for (int q = 0; q < ds; ++q) common |= stage[q] == eb.x;
+      if (common) w_defer(S, eb.x);
+      if (lane == 0) {
+        w_defer(S, b);
+        w_defer(S, s);
+      }
+      __syncwarp();  // stage is reused by the caller
+    }
+  }
+  // age_incident_edges(b, +1, exclude s): the rows' entries other than s, in
+  // row order (the new b-s entry, appended, is the excluded one)
+  int n = 0;
+  if (created >= 0) {
+    bool cross = false;
+    if (lane < db && eb.x != s) {
+      const int nw = ag + 1;
+      S.eage[eb.y] = nw;
+      cross = nw > P.max_age && ag <= P.max_age;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, cross);
+    if (cross) over[__popc(bal & ((1u << lane) - 1u))] = eb.x;
+    n = __popc(bal);
+  }
+  if (lane == 0) *nover = n;
+  // moves: the winner, its neighbours (the rows as they stand now: s joined
+  // them if the edge was created)
+  if (lane == 0) {
+    move_toward(pb, P.eps_b, x, y, z);
+    S.pos[b] = pb;
+    const double h0 = hb;
+    hb = dmul(h0, P.c_b);
+    S.hab[b] = hb;
+    if (h0 >= P.h_t && hb < P.h_t) atomicSub(&c->untrained, 1);
+    if (created == 1) {
+      move_toward(ps, P.eps_n, x, y, z);
+      S.pos[s] = ps;
+      const double h1 = dmul(hs, P.c_n);
+      S.hab[s] = h1;
+      if (hs >= P.h_t && h1 < P.h_t) atomicSub(&c->untrained, 1);
+    }
+  }
+  if (lane < db) {
+    move_toward(pv, P.eps_n, x, y, z);
+    S.pos[eb.x] = pv;
+    const double h1 = dmul(hv, P.c_n);
+    S.hab[eb.x] = h1;
+    if (hv >= P.h_t && h1 < P.h_t) atomicSub(&c->untrained, 1);
+  }
+  __syncwarp();
 }
 
 // habituation of neighbour v (untrained at the window start, hvT) at the
@@ -835,6 +969,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
   __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
+  __shared__ int s_defer_sm[kDeferSm];  // deferred ring recomputes (event path)
   __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
   // this CTA's processed signals of the window, compacted in batch order:
   // processed signal k of the CTA is evaluated (B, C1) by thread k, while
@@ -1175,6 +1310,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           Counters* cc = &s_cnt;
           DevState SD = S;
           SD.defer_n = &s_defer_n;
+          SD.defer_sm = s_defer_sm;
           SD.cnt = cc;
           const WinRec r = rec[jstar];
           const double x = sig[3 * (size_t)jstar], y = sig[3 * (size_t)jstar + 1],
@@ -1186,32 +1322,55 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
             cc->events++;
             cc->stale_n = 0;
           }
-          w_event_part1a(SD, P, r.b, r.s, s_over, &s_i[3], s_stage);
-          // winner and neighbours move / decay: independent units, one lane each
-          if (lane == 0) {
-            double4 p = S.pos[r.b];
-            move_toward(p, P.eps_b, x, y, z);
-            S.pos[r.b] = p;
-            const double h0 = S.hab[r.b], h = dmul(h0, P.c_b);
-            S.hab[r.b] = h;
-            if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
-          }
-          int db;
-          const int2 e0 = row_lane(S, r.b, db);
-          const int2* B = S.adj + (size_t)r.b * kMaxDeg;
-          for (int k = lane; k < db; k += 32) {
-            const int v = k < 32 ? e0.x : B[k].x;
-            double4 p = S.pos[v];
-            move_toward(p, P.eps_n, x, y, z);
-            S.pos[v] = p;
-            const double h0 = S.hab[v], h = dmul(h0, P.c_n);
-            S.hab[v] = h;
-            if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
-          }
+#if GS_PROF_EV
           __syncwarp();
+          const long long te0 = clock64() + (r.b & 0) + (long long)(x * 0.0);
+          if (lead) acc[3] += te0 - t_ser;  // counters in + record / signal
+#endif
+          // the winner's and the second's rows (one load level) decide the path
+          int rdb, rds;
+          const int2 reb = row_lane(S, r.b, rdb);
+          const int2 res = row_lane(S, r.s, rds);
+          double thb = 0.0, hb = 0.0;
+          double4 pb = make_double4(0.0, 0.0, 0.0, 0.0);
+          if (rdb < 32 && rds < 32) {
+            w_event_first(SD, P, r.b, r.s, x, y, z, rdb, reb, rds, res, s_over, &s_i[3], s_stage,
+                          thb, hb, pb);
+          } else {
+            w_event_part1a(SD, P, r.b, r.s, s_over, &s_i[3], s_stage);
+            // winner and neighbours move / decay: independent units, one lane each
+            if (lane == 0) {
+              pb = S.pos[r.b];
+              move_toward(pb, P.eps_b, x, y, z);
+              S.pos[r.b] = pb;
+              const double h0 = S.hab[r.b];
+              hb = dmul(h0, P.c_b);
+              S.hab[r.b] = hb;
+              thb = S.theta[r.b];
+              if (h0 >= P.h_t && hb < P.h_t) atomicSub(&cc->untrained, 1);
+            }
+            int db;
+            const int2 e0 = row_lane(S, r.b, db);
+            const int2* B = S.adj + (size_t)r.b * kMaxDeg;
+            for (int k = lane; k < db; k += 32) {
+              const int v = k < 32 ? e0.x : B[k].x;
+              double4 p = S.pos[v];
+              move_toward(p, P.eps_n, x, y, z);
+              S.pos[v] = p;
+              const double h0 = S.hab[v], h = dmul(h0, P.c_n);
+              S.hab[v] = h;
+              if (h0 >= P.h_t && h < P.h_t) atomicSub(&cc->untrained, 1);
+            }
+            __syncwarp();
+          }
+#if GS_PROF_EV
+          if (lead) acc[10] += clock64() - te0;  // touch + connect + age + moves
+#endif
+          thb = __shfl_sync(0xffffffffu, thb, 0);
+          hb = __shfl_sync(0xffffffffu, hb, 0);
           const long long t_mid = clock64();
           const int fired = w_event_part1b(SD, P, r.b, r.s, r.dwin, x, y, z, s_over, s_i[3],
-                                           s_stage);
+                                           s_stage, thb, hb, pb);
           if (lane == 0) {
             const long long t_end = clock64();
             acc[4] += t_mid - t_ser;  // event: connect/age + moves
@@ -1230,10 +1389,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         }
         __syncthreads();
         const long long t_rc = clock64();
-        // deferred ring reclassification, one warp per affected unit
-        const int nd = min(s_defer_n, kDeferCap);
+        // deferred ring reclassification, one warp per affected unit (an
+        // entry repeated earlier in the list is skipped)
+        const int nd = min(s_defer_n, kDeferSm + kDeferCap);
         for (int i = warp; i < nd; i += kUpdThreads / 32) {
-          const int u = S.defer_list[i];
+          const int u = defer_at(S, s_defer_sm, i);
+          bool dup = false;
+          for (int q0 = 0; q0 < i; q0 += 32)
+            dup |= q0 + lane < i && defer_at(S, s_defer_sm, q0 + lane) == u;
+          if (__any_sync(0xffffffffu, dup)) continue;
           if (S.alive[u]) {
             const int nw = classify_ring_warp(S, u, s_ring_sh[warp]);
             if (lane == 0) {
@@ -1245,7 +1409,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
               }
             }
           }
-          if (lane == 0) S.touchfirst[u] = kNone32;
         }
         __syncthreads();
         if (tid == 0) acc[1] += clock64() - t_rc;  // event: ring reclassification
@@ -1437,12 +1600,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     st->halted = c->halted;
     for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
 #ifdef GS_PROF_TL
-    if (batch_no >= GS_PROF_TL && batch_no < GS_PROF_TL + 3) {
+    {
       unsigned long long tl2;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
-      unsigned smid;
-      asm("mov.u32 %0, %%smid;" : "=r"(smid));
-      printf("U %d %u %llu %llu %llu %lld\n", batch_no, smid, tl0, tl1, tl2, c->windows);
+      unsigned long long* g = g_tlu[batch_no & 8191];
+      g[0] = tl0;
+      g[1] = tl1;
+      g[2] = tl2;
     }
 #endif
     // the host's ring slot (pinned, mapped): no copy between the kernels
