@@ -57,8 +57,18 @@ __device__ __forceinline__ void stage_adj(const int2* A, int d, int2 (&nb)[kStag
   }
 }
 
+// the event path's functions out of line (fewer spills in B / the walk, but
+// measured slower: cfg3 395 vs 382 ms, the calls sit on the event's latency)
+#ifndef GS_EV_NOINLINE
+#define GS_EV_NOINLINE 0
+#endif
+#if GS_EV_NOINLINE
+#define GS_EVNOINLINE __noinline__
+#else
+#define GS_EVNOINLINE
+#endif
 #ifndef GS_OPT_STAGEALL_B
-#define GS_OPT_STAGEALL_B 0
+#define GS_OPT_STAGEALL_B 1
 #endif
 #ifndef GS_OPT_STAGEALL_W
 #define GS_OPT_STAGEALL_W 0
@@ -540,7 +550,7 @@ __device__ void w_prune_winner(const DevState& S, const Params& P, int b, const 
 
 // sweep clock (no stale units to remove) + adapt_threshold (engine.py:208-238,
 // 345-355), whole warp: the neighbours' habituation is checked lane-parallel
-__device__ void w_event_part2(const DevState& S, const Params& P, int b, bool sweep_fired) {
+__device__ GS_EVNOINLINE void w_event_part2(const DevState& S, const Params& P, int b, bool sweep_fired) {
   const int lane = threadIdx.x & 31;
   Counters* c = S.cnt;
   if (lane == 0 && sweep_fired) c->next_sweep = c->tick + kSweepEvery;
@@ -568,7 +578,7 @@ __device__ void w_event_part2(const DevState& S, const Params& P, int b, bool sw
 }
 
 // update_single up to the edge aging (engine.py:303-308), whole warp
-__device__ void w_event_part1a(const DevState& S, const Params& P, int b, int s, int* over,
+__device__ GS_EVNOINLINE void w_event_part1a(const DevState& S, const Params& P, int b, int s, int* over,
                                int* nover, int* stage) {
   const int lane = threadIdx.x & 31;
   Counters* c = S.cnt;
@@ -591,7 +601,7 @@ __device__ void w_event_part1a(const DevState& S, const Params& P, int b, int s,
 // clock fired (uniform)
 // (thb, hb, wp: the winner's threshold, habituation and position after its
 // move, as the first part left them)
-__device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, double dw,
+__device__ GS_EVNOINLINE int w_event_part1b(const DevState& S, const Params& P, int b, int s, double dw,
                               double x, double y, double z, const int* over, int nover,
                               int* stage, double thb, double hb, const double4& wp) {
   const int lane = threadIdx.x & 31;
@@ -637,7 +647,7 @@ __device__ int w_event_part1b(const DevState& S, const Params& P, int b, int s, 
 // (network.py:294-319, over-age neighbours in row order) and the moves run on
 // registers.  Whole warp, uniform arguments; lane 0's thb / hb / pb: the
 // winner's threshold, habituation and position afterwards.
-__device__ void w_event_first(const DevState& S, const Params& P, int b, int s, double x,
+__device__ GS_EVNOINLINE void w_event_first(const DevState& S, const Params& P, int b, int s, double x,
                               double y, double z, int db, int2 eb, int ds, int2 es, int* over,
                               int* nover, int* stage, double& thb, double& hb, double4& pb) {
   const int lane = threadIdx.x & 31;
