@@ -885,6 +885,13 @@ struct gs_engine {
   // per-batch stats copies (ring of pinned slots + completion events) so the
   // host can read batch i - lag while later batches are still queued
   gs_batch_stats* h_ring = nullptr;
+  // the update kernel writes each batch's stats into a device ring slot (a
+  // host-mapped write would sit on the kernel's completion, i.e. on the next
+  // find's release); batches the host will read are copied to h_ring on a
+  // copy stream behind their completion event
+  gs_batch_stats* d_ring = nullptr;
+  cudaStream_t cp = nullptr;
+  cudaEvent_t cp_ev[64] = {};
   cudaEvent_t stat_ev[64] = {};
   int64_t issued = 0;
   int64_t reset_seq = 0;     // steps issued before the last reset (stale for lagged reads)
@@ -1250,6 +1257,10 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
       e->h_ring = (gs_batch_stats*)hmalloc(sizeof(gs_batch_stats) * gs_engine::kEvRing);
       memset(e->h_ring, 0, sizeof(gs_batch_stats) * gs_engine::kEvRing);
       for (auto& ev : e->stat_ev) GS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      for (auto& ev : e->cp_ev) GS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      e->d_ring = (gs_batch_stats*)dmalloc(sizeof(gs_batch_stats) * gs_engine::kEvRing, st);
+      GS_CUDA(cudaMemsetAsync(e->d_ring, 0, sizeof(gs_batch_stats) * gs_engine::kEvRing, st));
+      GS_CUDA(cudaStreamCreateWithFlags(&e->cp, cudaStreamNonBlocking));
       for (auto& b : e->stat_batch) b = -1;
       e->d_res = (long long*)dmalloc(4 * sizeof(long long), st);
       e->h_res = (long long*)hmalloc(4 * sizeof(long long));
@@ -1273,7 +1284,13 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.ttr, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
-                  S.rowpos, S.rowf};
+                  S.rowpos, S.rowf, e->d_ring};
+  if (e->cp) {
+    cudaStreamSynchronize(e->cp);
+    cudaStreamDestroy(e->cp);
+  }
+  for (auto ev : e->cp_ev)
+    if (ev) cudaEventDestroy(ev);
   for (void* q : ptrs) dfree(q, e->stream);  // stream is idle: back to the pool at once
   hfree(e->h_stats);
   hfree(e->h_ring);
@@ -1456,10 +1473,10 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
     launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
     if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
   }
-  // the kernel writes its stats straight into the host ring slot (pinned,
-  // mapped under UVA): no copy between this batch's kernels and the next
+  // the kernel writes its stats into the device ring slot; no copy between
+  // this batch's kernels and the next
   const int slot = (int)(e->issued % gs_engine::kEvRing);
-  launch_update(e, d_sig, rec, m, e->h_ring + slot);
+  launch_update(e, d_sig, rec, m, e->d_ring + slot);
   if (timed) {
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;
@@ -1468,6 +1485,10 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
   // between two kernels and stops the programmatic overlap there)
   if (mark) {
     GS_CUDA(cudaEventRecord(e->stat_ev[slot], e->stream));
+    GS_CUDA(cudaStreamWaitEvent(e->cp, e->stat_ev[slot], 0));
+    GS_CUDA(cudaMemcpyAsync(e->h_ring + slot, e->d_ring + slot, sizeof(gs_batch_stats),
+                            cudaMemcpyDeviceToHost, e->cp));
+    GS_CUDA(cudaEventRecord(e->cp_ev[slot], e->cp));
     e->stat_batch[slot] = e->issued;
   }
   e->issued++;
@@ -1530,7 +1551,8 @@ extern "C" gs_status gs_engine_phase_ms(gs_engine* e, int enable, double out[2])
 // newest device-step stats into h_stats (after the stream is idle)
 void latest_stats(gs_engine* e) {
   if (e->ring_latest && e->issued > 0)
-    *e->h_stats = e->h_ring[(e->issued - 1) % gs_engine::kEvRing];
+    GS_CUDA(cudaMemcpy(e->h_stats, e->d_ring + (e->issued - 1) % gs_engine::kEvRing,
+                       sizeof(gs_batch_stats), cudaMemcpyDeviceToHost));
 }
 
 extern "C" gs_status gs_engine_stats(gs_engine* e, gs_batch_stats* out) {
@@ -1565,7 +1587,7 @@ extern "C" gs_status gs_engine_stats_lagged(gs_engine* e, int64_t lag, gs_batch_
       memset(out, 0, sizeof(*out));
       return;
     }
-    GS_CUDA(cudaEventSynchronize(e->stat_ev[target % gs_engine::kEvRing]));
+    GS_CUDA(cudaEventSynchronize(e->cp_ev[target % gs_engine::kEvRing]));
     // per-phase timings of the batches known complete (up to target)
     while (e->ev_count > 0 && e->ev_b[e->ev_head] <= target) {
       fold_timing_entry(e);

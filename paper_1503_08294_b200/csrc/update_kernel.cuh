@@ -1620,7 +1620,11 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
 #endif
     // the host's ring slot (pinned, mapped): no copy between the kernels
+#ifndef GS_NO_HOST_STATS
     if (st_out != st) {
+#else
+    if (false) {
+#endif
       *st_out = *st;
 #if GS_STATS_FENCE
       __threadfence_system();  // (the host reads the slot only after an event)
