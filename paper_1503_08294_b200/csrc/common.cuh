@@ -255,6 +255,11 @@ struct FindArgs {
   WinRec* out_win = nullptr;
   int mode = GS_FIND_AUTO;
   int tl_batch = -1;             // timeline profiling builds: the update batch this feeds
+  // the engine's own batches: the record epilogue also marks each winner's
+  // first signal (atomicMin) for signals < fw_limit -- the update kernel's
+  // first window then starts with its candidates resolved
+  int32_t* firstwin = nullptr;
+  int64_t fw_limit = 0;
 };
 
 // row r of a find's unit set (false: a dead engine slot)
@@ -288,6 +293,8 @@ __device__ __forceinline__ void write_result(const FindArgs& a, int64_t j, const
     w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
     w.dwin = __dsqrt_rn(b.d1);  // math.sqrt (correctly rounded): multi.py:72-78
     a.out_win[j] = w;
+    if (a.firstwin && j < a.fw_limit && w.b >= 0 && w.s >= 0 && w.b != w.s)
+      atomicMin(&a.firstwin[w.b], (int32_t)j);
   }
 }
 

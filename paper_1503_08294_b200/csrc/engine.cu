@@ -106,6 +106,11 @@ struct Counters {
   int rowpos_n;  // rows described by rowpos (-1: stale, the find gathers through rows)
   int deaths;    // units removed so far (an event without deaths lets the window resume)
   long long ev_cutoff;
+  // minimum last_active over live units at the end of a batch (the tail
+  // computes it for the next one; slot batch_no & 1 is read, the other
+  // written): the silent-sweep test's value for a first window the find
+  // resolved
+  long long minla_next[2];
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
   // FP32 unit pairs of the row snapshot (the screened find's staging): centre
@@ -1134,7 +1139,7 @@ long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
 }
 
 void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m,
-                   gs_batch_stats* st_out = nullptr) {
+                   gs_batch_stats* st_out = nullptr, bool pre_fw = false) {
   if constexpr (kCluster > 8) {  // clusters beyond the portable 8 CTAs need an opt-in
     static bool opted = false;
     if (!opted) {
@@ -1153,14 +1158,15 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   GS_CUDA(cudaLaunchKernelEx(&cfg, k_update_batch, e->S, e->P, d_sig, d_rec, (int)m, e->batch_no,
-                             st_out ? st_out : e->S.stats));
+                             pre_fw ? 1 : 0, st_out ? st_out : e->S.stats));
   GS_CUDA(cudaGetLastError());
   e->launches++;
   ++g_launches;
 }
 
 void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinRec* d_rec,
-                 const int64_t* sig_idx = nullptr, const double* sig_pts = nullptr) {
+                 const int64_t* sig_idx = nullptr, const double* sig_pts = nullptr,
+                 bool pre_fw = false) {
   GS_CHECK(e->n_units >= 2, GS_STATE_ERROR, "need at least 2 units to find winners");
   FindArgs a;
   a.pos4 = e->S.pos;
@@ -1187,6 +1193,10 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   a.out_win = d_rec + lo;
   a.mode = e->hp.find_mode;
   a.tl_batch = e->batch_no + 1;  // the update this find feeds (timeline builds)
+  if (pre_fw) {  // the whole batch on this engine: resolve the first window's candidates
+    a.firstwin = e->S.firstwin;
+    a.fw_limit = kWinC;
+  }
   const unsigned long long before = g_launches;
   find_launch(*e->ctx, a, e->stream, e->find_work);
   e->launches += (long long)(g_launches - before);
@@ -1470,13 +1480,13 @@ void step_device_impl(gs_engine* e, const double* d_sig, int64_t m, const int64_
     GS_CHECK(r == ncclSuccess, GS_CUDA_ERROR, std::string("ncclAllGather: ") + ncclGetErrorString(r));
     if (timed) GS_CUDA(cudaEventRecord(evs[3], e->stream));
   } else {
-    launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts);
+    launch_find(e, d_sig, 0, m, rec, sig_idx, sig_pts, true);
     if (timed) GS_CUDA(cudaEventRecord(evs[1], e->stream));
   }
   // the kernel writes its stats into the device ring slot; no copy between
   // this batch's kernels and the next
   const int slot = (int)(e->issued % gs_engine::kEvRing);
-  launch_update(e, d_sig, rec, m, e->d_ring + slot);
+  launch_update(e, d_sig, rec, m, e->d_ring + slot, e->comm == nullptr);
   if (timed) {
     GS_CUDA(cudaEventRecord(evs[2], e->stream));
     e->ev_count++;

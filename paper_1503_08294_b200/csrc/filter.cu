@@ -328,6 +328,8 @@ __device__ __forceinline__ void write_best(const FindArgs& a, int64_t j, const B
     w.s = (b.i2 >= 0 && a.rows) ? a.rows[b.i2] : b.i2;
     w.dwin = __dsqrt_rn(b.d1);  // math.sqrt: multi.py:72-78
     a.out_win[j] = w;
+    if (a.firstwin && j < a.fw_limit && w.b >= 0 && w.s >= 0 && w.b != w.s)
+      atomicMin(&a.firstwin[w.b], (int32_t)j);
   }
 }
 

@@ -968,7 +968,7 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 #endif
 __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     k_update_batch(DevState S, Params P, const double* __restrict__ sig,
-                   const WinRec* __restrict__ rec, int m, int batch_no,
+                   const WinRec* __restrict__ rec, int m, int batch_no, int pre_fw,
                    gs_batch_stats* st_out) {
   __shared__ int s_warp[33];
   __shared__ long long s_ll32[33];
@@ -1007,9 +1007,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (S.cnt->halted) {  // converged earlier in an asynchronous run (uniform)
     // the batch's stats slot still gets the (unchanged) latest values
-    if (st_out != S.stats && threadIdx.x == 0 && crank_of() == 0) {
-      *st_out = *S.stats;
-      __threadfence_system();
+    if (st_out != S.stats && threadIdx.x == 0 && crank_of() == 0) *st_out = *S.stats;
+    if (pre_fw) {  // undo the find's first-signal marks
+      const int g0 = crank_of() * kUpdThreads + threadIdx.x;
+      if (g0 < m) {
+        const int b = rec[g0].b;
+        if (b >= 0) S.firstwin[b] = kNone32;
+      }
     }
     return;
   }
@@ -1021,6 +1025,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #pragma unroll
   for (int q = 0; q < 13; ++q) acc[q] = 0;
   if (lead) {
+    c->minla_next[(batch_no + 1) & 1] = 0x7fffffffffffffffLL;  // the tail's atomicMin target
     c->processed = c->discarded = c->events = c->windows = 0;
     c->inserted_start = c->next_id;
     c->stale_n = 0;
@@ -1060,7 +1065,11 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       const int next_id = c->next_id;
       tick0 = c->tick;
       const long long next_sweep0 = c->next_sweep;
-      // ---- A: candidates; the first candidate per winner is processed
+      // ---- A: candidates; the first candidate per winner is processed.  In
+      //      the batch's first window after the engine's own find, the find
+      //      resolved them (its records are of live, distinct units, nothing
+      //      is claimed yet, and it marked every winner's first signal).
+      const bool pre = pre_fw && j0 == 0;
       const int j = j0 + g;
       cand = false;
       cb = -1;
@@ -1069,20 +1078,30 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         cb = r.b;
         my_s = r.s;
         my_dw = r.dwin;
-        cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
-               S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
-        if (cand) atomicMin(&S.firstwin[r.b], j);
-      }
-      // minimum last_active over live units (silent-sweep test), window start;
-      // it only grows, so later segments may use this (conservative) value
-      long long mla = 0x7fffffffffffffffLL;
-      if (tick0 + kWinC >= next_sweep0) {
-        for (int u = g; u < next_id; u += kWinC) {
-          const long long t = S.la_val[u];
-          if (t != -1 && S.alive[u] && t < mla) mla = t;
+        if (pre) {
+          cand = r.b >= 0 && r.s >= 0 && r.b != r.s;
+        } else {
+          cand = r.b >= 0 && r.s >= 0 && r.b < next_id && r.s < next_id && r.b != r.s &&
+                 S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
+          if (cand) atomicMin(&S.firstwin[r.b], j);
         }
       }
-      minla = cl_min_ll(mla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
+      if (pre) {
+        // minimum last_active over live units (silent-sweep test) as the
+        // previous batch left it
+        minla = c->minla_next[batch_no & 1];
+      } else {
+        // window start; it only grows, so later segments may use this
+        // (conservative) value
+        long long mla = 0x7fffffffffffffffLL;
+        if (tick0 + kWinC >= next_sweep0) {
+          for (int u = g; u < next_id; u += kWinC) {
+            const long long t = S.la_val[u];
+            if (t != -1 && S.alive[u] && t < mla) mla = t;
+          }
+        }
+        minla = cl_min_ll(mla, s_ll32, s_ctal, parity);  // cluster barrier: firstwin complete
+      }
       if (lead) { const long long t_ = clock64(); acc[0] += t_ - t_ph; t_ph = t_; }
       // every thread keeps its own signal: its processing rank (batch
       // order among the processed signals) is all the later phases need
@@ -1542,6 +1561,20 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
     if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits, __float_as_uint(pm));
+    // the next batch's silent-sweep value: minimum last_active over live units
+    long long mla = 0x7fffffffffffffffLL;
+    const int nid_e = c->next_id;
+    for (int u = g; u < nid_e; u += kWinC) {
+      const long long t = S.la_val[u];
+      if (t != -1 && S.alive[u] && t < mla) mla = t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const long long t = __shfl_xor_sync(0xffffffffu, mla, o);
+      mla = t < mla ? t : mla;
+    }
+    if ((tid & 31) == 0 && mla != 0x7fffffffffffffffLL)
+      atomicMin(&c->minla_next[(batch_no + 1) & 1], mla);
   }
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
