@@ -260,6 +260,11 @@ struct FindArgs {
   // first window then starts with its candidates resolved
   int32_t* firstwin = nullptr;
   int64_t fw_limit = 0;
+  // non-null: the preceding update publishes snap_target here once its row
+  // snapshot is complete (the screened find starts on it, not on the grid's
+  // completion; it still waits for that before it exits)
+  const int* snap_token = nullptr;
+  int snap_target = 0;
 };
 
 // row r of a find's unit set (false: a dead engine slot)

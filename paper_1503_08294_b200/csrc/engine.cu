@@ -111,6 +111,11 @@ struct Counters {
   // written): the silent-sweep test's value for a first window the find
   // resolved
   long long minla_next[2];
+  // row snapshot hand-off: every update CTA arrives once per launch after
+  // its part of the snapshot (monotone count); the last one publishes the
+  // launch's batch number in S.snap_token, on which the next find starts
+  // (before the update grid has drained)
+  int snap_arrive;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
   // FP32 unit pairs of the row snapshot (the screened find's staging): centre
@@ -156,6 +161,7 @@ struct DevState {
   int* defer_sm;        // the event path's shared-memory part of the deferred list
   Counters* cnt;
   gs_batch_stats* stats;
+  int* snap_token;  // own 128-byte line: the next find's CTAs poll it
   int U, EC;
   int rowf_stride;  // unit pairs per half of rowf (multiple of 64)
 };
@@ -1196,6 +1202,11 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   if (pre_fw) {  // the whole batch on this engine: resolve the first window's candidates
     a.firstwin = e->S.firstwin;
     a.fw_limit = kWinC;
+    // the previous kernel is this engine's update: start on its snapshot token
+    if (e->batch_no > 0) {
+      a.snap_token = e->S.snap_token;
+      a.snap_target = e->batch_no;
+    }
   }
   const unsigned long long before = g_launches;
   find_launch(*e->ctx, a, e->stream, e->find_work);
@@ -1259,6 +1270,8 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
       GS_CUDA(cudaMemcpyAsync(e->S.cnt, &init, sizeof(Counters), cudaMemcpyHostToDevice, e->stream));
       GS_CUDA(cudaStreamSynchronize(e->stream));
       e->S.stats = (gs_batch_stats*)dmalloc(sizeof(gs_batch_stats), st);
+      e->S.snap_token = (int*)dmalloc(128, st);
+      GS_CUDA(cudaMemsetAsync(e->S.snap_token, 0, 128, st));
       GS_CUDA(cudaMemsetAsync(e->S.stats, 0, sizeof(gs_batch_stats), st));
       e->S.aff = (int32_t*)dmalloc(sizeof(int32_t) * kAffCap, st);
       e->S.defer_list = (int32_t*)dmalloc(sizeof(int32_t) * kDeferCap, st);
@@ -1294,6 +1307,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
   void* ptrs[] = {S.pos, S.hab, S.theta, S.alive, S.ring, S.deg, S.adj, S.patience, S.la_val,
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.ttr, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
+                  S.snap_token,
                   S.rowpos, S.rowf, e->d_ring};
   if (e->cp) {
     cudaStreamSynchronize(e->cp);

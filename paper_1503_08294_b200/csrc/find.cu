@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
   __shared__ double s_d[kW][kSfCand];
   __shared__ double s_q[kW][kFS][3];
   __shared__ __align__(8) uint64_t s_bar;
+  __shared__ bool s_ok;
 #ifdef GS_PROF_TL
   unsigned long long tl[6] = {0, 0, 0, 0, 0, 0};
   SF_TL(0);
@@ -358,8 +359,27 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
   // launched as a programmatic dependent of the previous kernel (the update):
-  // every CTA may already be resident; wait for that grid's results here
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // every CTA may already be resident; start once the update's row snapshot
+  // is published (its token), or when that grid has completed
+  bool waited = false;
+  if (a.snap_token) {
+    if (threadIdx.x == 0) {
+      int spins = 0;
+      int t;
+      do {
+        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token) : "memory");
+        if (t - a.snap_target >= 0) break;
+        __nanosleep(64);
+      } while (++spins < (1 << 20));
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire after the token
+      s_ok = t - a.snap_target >= 0;
+    }
+    __syncthreads();
+    waited = !s_ok;
+  } else {
+    waited = true;
+  }
+  if (waited) asm volatile("griddepcontrol.wait;" ::: "memory");
   // ... and let the update (16 SMs) become resident on the SMs this grid
   // leaves free; it waits for this grid's records in turn
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -608,6 +628,8 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
       }
       if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&g_sf_seq, 1u);
 #endif
+      // complete only after the update grid has (the next update relies on it)
+      if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
       return;
     }
     full_scan = true;
@@ -629,6 +651,7 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
     if (lane == 0 && j < a.m) write_result(a, j, b[k]);
   }
   sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
+  if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // materialise sampled signals (sig[j] = pts[idx[j]]) for the non-fused finds

@@ -959,6 +959,23 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 }
 
 // ---------------------------------------------------------------------------
+// row-snapshot hand-off to the next find: each CTA arrives once per launch
+// after its writes the find reads (snapshot rows, counters); the launch's last
+// arrival publishes the batch number (release), see FindArgs::snap_token
+__device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(&S.cnt->snap_arrive, 1);
+    if ((old + 1) % kCluster == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token), "r"(batch_no)
+                   : "memory");
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // the batch update kernel: one cluster of kCluster CTAs (8 SMs)
 
 #if GS_CLUSTER > 1
@@ -1015,6 +1032,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         if (b >= 0) S.firstwin[b] = kNone32;
       }
     }
+    snapshot_arrive(S, batch_no);
     return;
   }
   const long long t_kernel = clock64();
@@ -1579,7 +1597,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
 #endif
-  if (crank != 0) return;
+  if (crank != 0) {
+    snapshot_arrive(S, batch_no);
+    return;
+  }
   if (tid == 0) c->rowpos_n = c->nrows;
   // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
   if (c->ndead_rows * 8 > c->nrows) {
@@ -1601,7 +1622,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       c->ndead_rows = 0;
     }
   }
-  __syncthreads();
+  snapshot_arrive(S, batch_no);  // (includes the block barrier)
 #if GS_PROF_TAIL
   if (tid == 0) {
     const long long tt3 = clock64();
