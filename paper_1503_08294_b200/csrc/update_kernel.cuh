@@ -975,6 +975,25 @@ __device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no)
   }
 }
 
+// the next batch's silent-sweep value: minimum last_active over live units
+// (after the snapshot hand-off: only the next update reads it)
+__device__ __forceinline__ void next_minla(const DevState& S, int batch_no, int g) {
+  Counters* c = S.cnt;
+  long long mla = 0x7fffffffffffffffLL;
+  const int nid_e = c->next_id;
+  for (int u = g; u < nid_e; u += kWinC) {
+    const long long t = S.la_val[u];
+    if (t != -1 && S.alive[u] && t < mla) mla = t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long t = __shfl_xor_sync(0xffffffffu, mla, o);
+    mla = t < mla ? t : mla;
+  }
+  if ((threadIdx.x & 31) == 0 && mla != 0x7fffffffffffffffLL)
+    atomicMin(&c->minla_next[(batch_no + 1) & 1], mla);
+}
+
 // ---------------------------------------------------------------------------
 // the batch update kernel: one cluster of kCluster CTAs (8 SMs)
 
@@ -1579,26 +1598,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
     if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits, __float_as_uint(pm));
-    // the next batch's silent-sweep value: minimum last_active over live units
-    long long mla = 0x7fffffffffffffffLL;
-    const int nid_e = c->next_id;
-    for (int u = g; u < nid_e; u += kWinC) {
-      const long long t = S.la_val[u];
-      if (t != -1 && S.alive[u] && t < mla) mla = t;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const long long t = __shfl_xor_sync(0xffffffffu, mla, o);
-      mla = t < mla ? t : mla;
-    }
-    if ((tid & 31) == 0 && mla != 0x7fffffffffffffffLL)
-      atomicMin(&c->minla_next[(batch_no + 1) & 1], mla);
   }
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
 #endif
   if (crank != 0) {
     snapshot_arrive(S, batch_no);
+    next_minla(S, batch_no, g);
     return;
   }
   if (tid == 0) c->rowpos_n = c->nrows;
@@ -1623,6 +1629,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
   }
   snapshot_arrive(S, batch_no);  // (includes the block barrier)
+  next_minla(S, batch_no, g);
 #if GS_PROF_TAIL
   if (tid == 0) {
     const long long tt3 = clock64();
