@@ -121,6 +121,25 @@ _lib = None
 _lock = threading.Lock()
 
 
+def _preload_nccl() -> None:
+    """Load the NCCL that PyTorch ships (the nvidia-nccl wheel), if present,
+    before the library: the library links libnccl.so.2 by soname, so both then
+    share that copy.  Loaded the other way round, the system's older NCCL
+    would satisfy the soname first and a later ``import torch`` would fail
+    (libtorch_cuda needs symbols it lacks)."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        f = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(f):
+            C.CDLL(f, mode=C.RTLD_GLOBAL)
+            return
+
+
 def load_library(path: str = LIB_PATH):
     """Load the shared library and declare every symbol (no device needed)."""
     global _lib
@@ -130,6 +149,7 @@ def load_library(path: str = LIB_PATH):
                 raise DeviceUnavailable(
                     f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
                     "g.build()'` (nvcc, sm_100a)")
+            _preload_nccl()
             lib = C.CDLL(path)
             for name, (res, args) in _SIGNATURES.items():
                 fn = getattr(lib, name)

@@ -358,6 +358,29 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
     fence_barrier_init();
   }
   __syncthreads();  // the barrier is initialised before anyone waits on it
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t sig0 = ((int64_t)blockIdx.x * kW + warp) * kFS;
+  // signals (FP64, as the reference reads them): the sampled indices and the
+  // cloud do not depend on the update, so the gather overlaps it (the
+  // engine's signal buffer is written only at the end, after the update)
+  double qx[kFS], qy[kFS], qz[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const int64_t j = sig0 + k;
+    qx[k] = qy[k] = qz[k] = 0.0;
+    if (j < a.m) {
+      if (a.sig_idx) {  // fused sampling: gather (stored for the update at the end)
+        const size_t src = 3 * (size_t)a.sig_idx[j];
+        qx[k] = a.sig_pts[src];
+        qy[k] = a.sig_pts[src + 1];
+        qz[k] = a.sig_pts[src + 2];
+      } else {
+        qx[k] = a.sig[3 * j];
+        qy[k] = a.sig[3 * j + 1];
+        qz[k] = a.sig[3 * j + 2];
+      }
+    }
+  }
   // launched as a programmatic dependent of the previous kernel (the update):
   // every CTA may already be resident; start once the update's row snapshot
   // is published (its token), or when that grid has completed
@@ -394,29 +417,8 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
     tma_bulk_g2s(A1, a.rowf + a.rowf_stride, 16u * (uint32_t)ncopy, &s_bar);
   }
   const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t sig0 = ((int64_t)blockIdx.x * kW + warp) * kFS;
   const bool compact = a.rowpos && *a.rowpos_n == n;
 
-  // signals (FP64, as the reference reads them)
-  double qx[kFS], qy[kFS], qz[kFS];
-#pragma unroll
-  for (int k = 0; k < kFS; ++k) {
-    const int64_t j = sig0 + k;
-    qx[k] = qy[k] = qz[k] = 0.0;
-    if (j < a.m) {
-      if (a.sig_idx) {  // fused sampling: gather (stored for the update at the end)
-        const size_t src = 3 * (size_t)a.sig_idx[j];
-        qx[k] = a.sig_pts[src];
-        qy[k] = a.sig_pts[src + 1];
-        qz[k] = a.sig_pts[src + 2];
-      } else {
-        qx[k] = a.sig[3 * j];
-        qy[k] = a.sig[3 * j + 1];
-        qz[k] = a.sig[3 * j + 2];
-      }
-    }
-  }
   bool full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
   // the copies complete on the mbarrier whatever path follows
   if (tma) mbar_wait(&s_bar, 0);

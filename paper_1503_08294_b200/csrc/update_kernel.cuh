@@ -658,8 +658,9 @@ __device__ GS_EVNOINLINE void w_event_first(const DevState& S, const Params& P, 
   double4 ps = make_double4(0.0, 0.0, 0.0, 0.0);
   double hs = 0.0;
   int enext = -1;
-  const int top = c->efree_top;
+  int top = 0;  // lane 0's (the only lane that uses or moves the free-edge stack)
   if (lane == 0) {
+    top = c->efree_top;
     pb = S.pos[b];
     hb = S.hab[b];
     thb = S.theta[b];
@@ -877,6 +878,18 @@ __device__ __forceinline__ void csync() {
     cg::this_cluster().sync();
   }
 }
+// split cluster barrier (no memory ordering on the arrive): the kernel's
+// start-up barrier overlaps the first window's loads
+__device__ __forceinline__ void carrive_relaxed() {
+  if constexpr (kCluster > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cwait() {
+  if constexpr (kCluster == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
+}
 template <class T>
 __device__ __forceinline__ T* cmap(T* p, int rank) {
   if constexpr (kCluster == 1) {
@@ -1069,7 +1082,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->nwalk = 0;
     c->fpm_bits = 0u;
   }
-  csync();
+  // every CTA of the cluster must have started before the first DSMEM
+  // exchange; the lead's resets above are read only after later barriers
+  carrive_relaxed();
+  bool start_wait = true;
   int j0 = 0;
   // A window [j0, wend) is evaluated once (A: candidates, scan: processed
   // list by rank) and committed in segments of ranks [rbase, r*): after an
@@ -1122,6 +1138,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
                  S.alive[r.b] && S.alive[r.s] && S.claim[r.b] != batch_no;
           if (cand) atomicMin(&S.firstwin[r.b], j);
         }
+      }
+      if (start_wait) {
+        cwait();
+        start_wait = false;
       }
       if (pre) {
         // minimum last_active over live units (silent-sweep test) as the
@@ -1533,6 +1553,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #if GS_PROF_TAIL
   const long long tt0 = clock64();
 #endif
+  if (start_wait) cwait();  // (no window ran: m == 0)
   csync();  // the last window's walk stores are visible to the snapshot below
 #if GS_PROF_TAIL
   const long long tt1 = clock64();

@@ -102,3 +102,15 @@ def test_mesh_metrics_euler_anchors():
 
     assert euler_genus(347, 1035, 690) == 0
     assert euler_genus(658, 1980, 1320) == 2
+
+
+def test_library_then_torch_import_order():
+    """Loading the library before torch must not break torch: the library
+    links libnccl.so.2 by soname and _lib preloads the NCCL torch ships."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r); from paper_1503_08294_b200 import _lib; "
+            "_lib.load_library(); import torch; print('ok')" % REPO)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
