@@ -265,6 +265,17 @@ struct FindArgs {
   // completion; it still waits for that before it exits)
   const int* snap_token = nullptr;
   int snap_target = 0;
+  // speculative screen (the screened find, engine batches): the snapshot
+  // before the preceding update (its FP32 pairs, centre, max-norm, rows) and
+  // the row generations / largest displacements of both snapshots
+  const float4* rowf_prev = nullptr;
+  const double* fcen_prev = nullptr;
+  const unsigned* fpm_prev = nullptr;
+  const int* rowpos_n_prev = nullptr;
+  const int* gen_prev = nullptr;
+  const int* gen_cur = nullptr;
+  const unsigned* disp_prev = nullptr;
+  const unsigned* disp_cur = nullptr;
 };
 
 // row r of a find's unit set (false: a dead engine slot)

@@ -103,7 +103,9 @@ struct Counters {
   int stale_n;
   int converged;
   int nwalk, defer_n, ev_fired, ev_b;
-  int rowpos_n;  // rows described by rowpos (-1: stale, the find gathers through rows)
+  // the row snapshot is double-buffered (slot = batch & 1: the next find
+  // reads the newest, its speculative screen the one before)
+  int rowpos_n[2];  // rows described by the slot (-1: stale, the find gathers through rows)
   int deaths;    // units removed so far (an event without deaths lets the window resume)
   long long ev_cutoff;
   // minimum last_active over live units at the end of a batch (the tail
@@ -120,8 +122,11 @@ struct Counters {
   long long batches;             // update kernels that ran (not halted)
   // FP32 unit pairs of the row snapshot (the screened find's staging): centre
   // (row 0 rounded to FP32) and max-norm of P' = fl32(p - centre), float bits
-  double fcen[3];
-  unsigned fpm_bits;
+  double fcen[2][3];
+  unsigned fpm_bits[2];
+  int row_gen;          // bumped by every change of the row list (insert, death, compaction)
+  int snap_gen[2];      // row_gen when the slot's snapshot was taken
+  unsigned snap_disp[2];  // float bits: max displacement of any row vs the other slot (inf: rows changed)
   unsigned prof_bmax[2];  // GS_PROF_B builds: slowest B / walk chain of the window (cycles)
   int pad_;
 };
@@ -151,6 +156,8 @@ struct DevState {
   int32_t* rows;        // row -> id (append-only, id order)
   double* rowpos;       // [3][U] row-ordered positions (dead rows +inf) for the find
   float4* rowf;         // [2][rowf_stride] FP32 unit pairs of the same rows (A0, A1)
+  const double* rowpos_prev;  // the other slot's rowpos (the tail's displacement bound)
+  int snap;             // snapshot slot this update writes
   int32_t* eage;        // [EC]
   int32_t* efree;       // [EC] free edge-id stack
   int32_t* iso_list;    // isolated units (network.py:93 _isolated)
@@ -335,6 +342,7 @@ __device__ int add_unit(const DevState& S, const Params& P, double x, double y, 
   c->n_units++;
   if (1.0 >= P.h_t) c->untrained++;
   S.rows[c->nrows++] = id;
+  c->row_gen++;
   return id;
 }
 
@@ -369,6 +377,7 @@ __device__ void remove_unit_raw(const DevState& S, const Params& P, int u) {
   iso_del(S, u);
   if (S.hab[u] >= P.h_t) c->untrained--;
   c->ndead_rows++;
+  c->row_gen++;
   c->deaths++;
 }
 
@@ -755,7 +764,7 @@ __device__ bool valid_unit(const DevState& S, int u) {
 
 __global__ void k_op(DevState S, Params P, OpArgs a, long long* res) {
   Counters* c = S.cnt;
-  c->rowpos_n = -1;  // positions / rows may change: the find gathers through rows
+  c->rowpos_n[0] = c->rowpos_n[1] = -1;  // positions / rows may change: the find gathers
   res[0] = 0;
   res[1] = 0;
   res[2] = 0;
@@ -901,6 +910,9 @@ struct gs_engine {
   // find's release); batches the host will read are copied to h_ring on a
   // copy stream behind their completion event
   gs_batch_stats* d_ring = nullptr;
+  double* rowpos_b[2] = {nullptr, nullptr};  // the two row-snapshot slots
+  bool spec_find = true;  // GS_SPEC_FIND=0 turns the speculative screen off
+  float4* rowf_b[2] = {nullptr, nullptr};
   cudaStream_t cp = nullptr;
   cudaEvent_t cp_ev[64] = {};
   cudaEvent_t stat_ev[64] = {};
@@ -1003,14 +1015,19 @@ void grow_units(gs_engine* e, int new_u) {
   grow_array(S.ttr, old, new_u, st);
   grow_array(S.iso_pos, old, new_u, st);
   grow_array(S.rows, old, new_u, st);
-  dfree(S.rowpos, st);  // regenerated by the next update (stride U)
-  S.rowpos = (double*)dmalloc(sizeof(double) * 3 * (size_t)new_u, st);
-  dfree(S.rowf, st);
   S.rowf_stride = ((new_u + 1) / 2 + 63) / 64 * 64;
-  S.rowf = (float4*)dmalloc(sizeof(float4) * 2 * (size_t)S.rowf_stride, st);
+  for (int k = 0; k < 2; ++k) {  // regenerated by the next updates (stride U)
+    dfree(e->rowpos_b[k], st);
+    e->rowpos_b[k] = (double*)dmalloc(sizeof(double) * 3 * (size_t)new_u, st);
+    dfree(e->rowf_b[k], st);
+    e->rowf_b[k] = (float4*)dmalloc(sizeof(float4) * 2 * (size_t)S.rowf_stride, st);
+  }
+  S.rowpos = e->rowpos_b[0];
+  S.rowf = e->rowf_b[0];
+  S.rowpos_prev = e->rowpos_b[1];
   {
-    const int stale = -1;
-    GS_CUDA(cudaMemcpyAsync(&S.cnt->rowpos_n, &stale, sizeof(int), cudaMemcpyHostToDevice, st));
+    const int stale2[2] = {-1, -1};
+    GS_CUDA(cudaMemcpyAsync(&S.cnt->rowpos_n[0], stale2, sizeof(stale2), cudaMemcpyHostToDevice, st));
     GS_CUDA(cudaStreamSynchronize(st));
   }
   grow_array(S.iso_list, old, new_u, st);
@@ -1154,6 +1171,13 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
     }
   }
   e->batch_no++;
+  {  // this update's row-snapshot slot
+    const int s = e->batch_no & 1;
+    e->S.snap = s;
+    e->S.rowpos = e->rowpos_b[s];
+    e->S.rowf = e->rowf_b[s];
+    e->S.rowpos_prev = e->rowpos_b[s ^ 1];
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kUpdThreads);
@@ -1186,12 +1210,12 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
   a.n = std::min<int64_t>(e->next_id, (int64_t)e->n_units + (e->n_units + 6) / 7 + 1);
   a.n_dev = &e->S.cnt->nrows;  // exact row count, read on the device
   a.rowpos = e->S.rowpos;
-  a.rowpos_n = &e->S.cnt->rowpos_n;
+  a.rowpos_n = &e->S.cnt->rowpos_n[e->S.snap];
   a.rowpos_stride = e->U;
   a.rowf = e->S.rowf;
   a.rowf_stride = e->S.rowf_stride;
-  a.fcen = e->S.cnt->fcen;
-  a.fpm_bits = &e->S.cnt->fpm_bits;
+  a.fcen = e->S.cnt->fcen[e->S.snap];
+  a.fpm_bits = &e->S.cnt->fpm_bits[e->S.snap];
   a.sig = d_sig + 3 * lo;
   a.sig_idx = sig_idx ? sig_idx + lo : nullptr;
   a.sig_pts = sig_pts;
@@ -1206,6 +1230,18 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
     if (e->batch_no > 0) {
       a.snap_token = e->S.snap_token;
       a.snap_target = e->batch_no;
+    }
+    if (e->batch_no > 1 && e->spec_find) {  // two snapshots exist: screen speculatively
+      const int cur = e->S.snap, prev = cur ^ 1;
+      Counters* c = e->S.cnt;
+      a.rowf_prev = e->rowf_b[prev];
+      a.fcen_prev = c->fcen[prev];
+      a.fpm_prev = &c->fpm_bits[prev];
+      a.rowpos_n_prev = &c->rowpos_n[prev];
+      a.gen_prev = &c->snap_gen[prev];
+      a.gen_cur = &c->snap_gen[cur];
+      a.disp_prev = &c->snap_disp[prev];
+      a.disp_cur = &c->snap_disp[cur];
     }
   }
   const unsigned long long before = g_launches;
@@ -1252,6 +1288,7 @@ extern "C" gs_status gs_engine_create(gs_ctx* ctx, const gs_params* p, int64_t c
     GS_CHECK(ctx && p && out, GS_VALUE_ERROR, "null argument");
     GS_CUDA(cudaSetDevice(ctx->device));
     gs_engine* e = new gs_engine();
+    if (const char* sp = getenv("GS_SPEC_FIND")) e->spec_find = atoi(sp) != 0;
     e->ctx = ctx;
     try {
       set_params(e, p);
@@ -1308,7 +1345,7 @@ extern "C" void gs_engine_destroy(gs_engine* e) {
                   S.la_stamp, S.claim, S.firstwin, S.touchfirst, S.ttr, S.iso_pos, S.rows, S.eage,
                   S.efree, S.iso_list, S.scratch, S.aff, S.defer_list, S.cnt, S.stats, e->d_res,
                   S.snap_token,
-                  S.rowpos, S.rowf, e->d_ring};
+                  e->rowpos_b[0], e->rowpos_b[1], e->rowf_b[0], e->rowf_b[1], e->d_ring};
   if (e->cp) {
     cudaStreamSynchronize(e->cp);
     cudaStreamDestroy(e->cp);

@@ -316,8 +316,12 @@ extern "C" int gs_debug_tl_find(unsigned long long* out, int n) {
 // the screen's threshold T = e2 + 2 f + slack, every operation rounded up
 // (an upper bound of the same expression evaluated exactly; filter.cu's
 // error bound with a = Pmax, Q = |q - c|)
+// delta > 0 (speculative screen against the snapshot before the last update,
+// delta >= every unit's displacement since): every unit whose distance may be
+// within the second-best one after the moves, i.e. old distance <= D2 + 2 delta
+// with D2 bounded by sqrt(e2 + f + Q^2):  T = (D2 + 2 delta)^2 - Q^2 + f
 __device__ __forceinline__ float sf_threshold(float e2, float pmaxf, double Qx, double Qy,
-                                              double Qz, bool& ok) {
+                                              double Qz, bool& ok, float delta = 0.f) {
   const float ax = __double2float_ru(fabs(Qx)), ay = __double2float_ru(fabs(Qy)),
               az = __double2float_ru(fabs(Qz));
   const float q2 = __fmaf_ru(az, az, __fmaf_ru(ay, ay, __fmul_ru(ax, ax)));
@@ -329,22 +333,130 @@ __device__ __forceinline__ float sf_threshold(float e2, float pmaxf, double Qx, 
   t = __fmaf_ru(__fmul_ru(6.02f * u, av), av, t);
   t = __fmaf_ru(__fmul_ru(8.03f * u, av), Q, t);
   const float fb = __fadd_ru(__fmul_ru(t, 1.0f + 1e-6f), 1e-38f);
+  if (delta > 0.f) {
+    const float qx = __double2float_rd(fabs(Qx)), qy = __double2float_rd(fabs(Qy)),
+                qz = __double2float_rd(fabs(Qz));
+    const float q2lo = __fmaf_rd(qz, qz, __fmaf_rd(qy, qy, __fmul_rd(qx, qx)));
+    const float d2 = __fsqrt_ru(fmaxf(0.f, __fadd_ru(__fadd_ru(e2, fb), q2)));
+    const float R = __fadd_ru(d2, __fmul_ru(2.0f, delta));
+    const float RR = __fmul_ru(R, R);
+    const float slack = __fmul_ru(1e-14f, __fadd_ru(RR, q2));
+    ok = ok && RR <= 1e30f;
+    return __fadd_ru(__fadd_ru(__fsub_ru(RR, q2lo), fb), slack);
+  }
   const float slack = __fmul_ru(1e-14f, __fadd_ru(__fadd_ru(fabsf(e2), fb), q2));
   return __fadd_ru(__fadd_ru(e2, __fmul_ru(2.0f, fb)), slack);
 }
 
+// pass 1 (lane minima of e), the thresholds and the candidate list of one
+// warp's kFS signals against nr staged rows (swizzled pairs A0 / A1, centre c,
+// max-norm pm); returns the candidate count, full_scan when the bound does
+// not apply
+template <int kFS>
+__device__ __forceinline__ int sf_screen(const float4* A0, const float4* A1, int nr, double cx,
+                                         double cy, double cz, float pm, float delta,
+                                         const double (&qx)[kFS], const double (&qy)[kFS],
+                                         const double (&qz)[kFS], int lane, int32_t* cand,
+                                         double (*sq)[3], bool& full_scan) {
+  // |p - c| <= sqrt(3) * max_k |P'_k| / (1 - u), rounded up generously
+  const float pmaxf = __fmul_ru(pm, 1.7320508075688774f * (1.0f + 1e-6f));
+  float2 fq[kFS][3];
+  float m1[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    const float fx = __double2float_rn(qx[k] - cx), fy = __double2float_rn(qy[k] - cy),
+                fz = __double2float_rn(qz[k] - cz);
+    fq[k][0] = make_float2(fx, fx);
+    fq[k][1] = make_float2(fy, fy);
+    fq[k][2] = make_float2(fz, fz);
+    m1[k] = INFINITY;
+  }
+  const int np64 = (((nr + 1) / 2) + 63) & ~63;  // padded pairs are +inf
+#pragma unroll 1
+  for (int p = lane; p < np64; p += 64) {
+    const int sa = sf_swz(p), sc = sf_swz(p + 32);
+    const float4 a0 = A0[sa], a1 = A1[sa];
+    const float4 c0 = A0[sc], c1 = A1[sc];
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) {
+      float2 ea = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
+      float2 ec = __ffma2_rn(make_float2(c0.x, c0.y), fq[k][0], make_float2(c1.z, c1.w));
+      ea = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], ea);
+      ec = __ffma2_rn(make_float2(c0.z, c0.w), fq[k][1], ec);
+      ea = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], ea);
+      ec = __ffma2_rn(make_float2(c1.x, c1.y), fq[k][2], ec);
+      m1[k] = fminf(m1[k], fminf(fminf(ea.x, ea.y), fminf(ec.x, ec.y)));
+    }
+  }
+  // screen: every signal's threshold (independent chains, issued together),
+  // then the surviving lanes' units one by one
+  float T[kFS];
+  unsigned tasks[kFS];
+#pragma unroll
+  for (int k = 0; k < kFS; ++k) {
+    float v1 = m1[k], v2 = INFINITY;  // two smallest lane minima
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float o1 = __shfl_xor_sync(0xffffffffu, v1, o);
+      const float o2 = __shfl_xor_sync(0xffffffffu, v2, o);
+      v2 = fminf(fmaxf(v1, o1), fminf(v2, o2));
+      v1 = fminf(v1, o1);
+    }
+    bool ok;
+    T[k] = sf_threshold(v2, pmaxf, qx[k] - cx, qy[k] - cy, qz[k] - cz, ok, delta);
+    full_scan |= !ok;  // warp-uniform
+    tasks[k] = __ballot_sync(0xffffffffu, m1[k] <= T[k]);
+  }
+  int cnt = 0;
+  if (!full_scan) {
+#pragma unroll
+    for (int k = 0; k < kFS; ++k) {
+      unsigned tk = tasks[k];
+      while (tk) {
+        const int l = __ffs(tk) - 1;
+        tk &= tk - 1;
+        for (int i0 = 0; i0 < np64 / 32; i0 += 32) {  // lane l's pairs l + 32 i, one per lane
+          const int p = 32 * (i0 + lane) + l;
+          const bool in = p < np64;
+          const int sp = sf_swz(p);  // conflict-free: lane i reads row i, column l ^ i
+          const float4 a0 = in ? A0[sp] : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 a1 = in ? A1[sp] : make_float4(0.f, 0.f, INFINITY, INFINITY);
+          float2 e = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
+          e = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], e);
+          e = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], e);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const bool pass = in && (h ? e.y : e.x) <= T[k];
+            const unsigned bal = __ballot_sync(0xffffffffu, pass);
+            const int at = cnt + __popc(bal & ((1u << lane) - 1u));
+            if (pass && at < kSfCand) cand[at] = ((2 * p + h) << 3) | k;
+            cnt += __popc(bal);
+          }
+        }
+      }
+      if (lane == 0) {
+        sq[k][0] = qx[k];
+        sq[k][1] = qy[k];
+        sq[k][2] = qz[k];
+      }
+    }
+  }
+  return cnt;
+}
+
 // kFS signals per warp, kW warps per CTA
 template <int kFS, int kW>
-__global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int tile_rows) {
+__global__ void __launch_bounds__(32 * kW, 2) find_small_f32_kernel(FindArgs a, int tile_rows) {
   static_assert(kFS == 1 || kFS == 2 || kFS == 4 || kFS == 8, "signals per warp");
   // A0[npad] {ax0,ax1,ay0,ay1}, A1[npad] {az0,az1,w0,w1}, pair p at sf_swz(p)
   extern __shared__ __align__(16) float4 s_u[];
   __shared__ float s_pm[kW];
   __shared__ int32_t s_cand[kW][kSfCand];  // (row << 3) | signal slot
   __shared__ double s_d[kW][kSfCand];
+  __shared__ int32_t s_cid[kW][kSfCand];  // speculative path: the candidates' unit ids
   __shared__ double s_q[kW][kFS][3];
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ bool s_ok;
+  __shared__ bool s_ok, s_verdict;
 #ifdef GS_PROF_TL
   unsigned long long tl[6] = {0, 0, 0, 0, 0, 0};
   SF_TL(0);
@@ -381,24 +493,62 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
       }
     }
   }
+  // ---- speculative screen (the engine's batches): while the update that
+  //      precedes runs, screen against the snapshot before it with the
+  //      threshold widened by a bound on that update's moves (twice the
+  //      previous update's largest displacement); after the update the
+  //      candidates stand if it changed no row and moved nothing further
+  bool spec = false;
+  float dspec = 0.f;
+  int n_prev = 0;
+  int cnt = 0;
+  bool full_scan = false;
+  uint32_t par = 0;
+  const int ncopy = (int)(npad < a.rowf_stride ? (int64_t)npad : a.rowf_stride);
+  if (a.rowf_prev && tma) {
+    n_prev = *a.rowpos_n_prev;
+    const float dprev = __uint_as_float(*a.disp_prev);
+    dspec = __fadd_ru(__fmul_ru(2.f, dprev), 1e-30f);
+    spec = n_prev >= 2 && n_prev <= tile_rows && dprev < 1e30f;  // (inf: rows changed)
+    if (spec) {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&s_bar, 2u * 16u * (uint32_t)ncopy);
+        tma_bulk_g2s(A0, a.rowf_prev, 16u * (uint32_t)ncopy, &s_bar);
+        tma_bulk_g2s(A1, a.rowf_prev + a.rowf_stride, 16u * (uint32_t)ncopy, &s_bar);
+      }
+      mbar_wait(&s_bar, 0);
+      par = 1;
+      cnt = sf_screen<kFS>(A0, A1, n_prev, a.fcen_prev[0], a.fcen_prev[1], a.fcen_prev[2],
+                           __uint_as_float(*a.fpm_prev), dspec, qx, qy, qz, lane, s_cand[warp],
+                           s_q[warp], full_scan);
+      // the candidates' unit ids now (the rows stand if the candidates do):
+      // the records need no row -> id load after the update
+      __syncwarp();
+      if (!full_scan && cnt <= kSfCand)
+        for (int c = lane; c < cnt; c += 32) s_cid[warp][c] = a.rows[s_cand[warp][c] >> 3];
+    }
+  }
   // launched as a programmatic dependent of the previous kernel (the update):
   // every CTA may already be resident; start once the update's row snapshot
   // is published (its token), or when that grid has completed
   bool waited = false;
+  bool verdict = false;  // the update's: the speculative candidates stand
   if (a.snap_token) {
     if (threadIdx.x == 0) {
       int spins = 0;
       int t;
       do {
         asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token) : "memory");
-        if (t - a.snap_target >= 0) break;
+        if ((t >> 1) - a.snap_target >= 0) break;
         __nanosleep(64);
       } while (++spins < (1 << 20));
       asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire after the token
-      s_ok = t - a.snap_target >= 0;
+      s_ok = (t >> 1) - a.snap_target >= 0;
+      s_verdict = s_ok && (t >> 1) == a.snap_target && (t & 1);
     }
     __syncthreads();
     waited = !s_ok;
+    verdict = s_verdict;
   } else {
     waited = true;
   }
@@ -407,22 +557,30 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
   // leaves free; it waits for this grid's records in turn
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   SF_TL(1);
-  // the update left the rows as swizzled FP32 unit pairs: two bulk copies of
-  // the whole tile (at most rowf_stride pairs) start before anything else;
-  // they are used only if that snapshot describes the current rows
-  const int ncopy = (int)(npad < a.rowf_stride ? (int64_t)npad : a.rowf_stride);
-  if (threadIdx.x == 0 && tma) {
-    mbar_expect_tx(&s_bar, 2u * 16u * (uint32_t)ncopy);
-    tma_bulk_g2s(A0, a.rowf, 16u * (uint32_t)ncopy, &s_bar);
-    tma_bulk_g2s(A1, a.rowf + a.rowf_stride, 16u * (uint32_t)ncopy, &s_bar);
+  // the speculative candidates hold if the update changed no row and moved
+  // none by more than the bound: its verdict, in the token (CTA-uniform)
+  const bool spec_ok = spec && verdict;
+  const int64_t n = spec_ok ? n_prev : a.n_dev ? (int64_t)*a.n_dev : a.n;
+  const bool compact = spec_ok || (a.rowpos && *a.rowpos_n == n);
+  if (!spec_ok) {
+    if (spec) {
+      full_scan = false;
+      cnt = 0;
+    }
+    // the update left the rows as swizzled FP32 unit pairs: two bulk copies of
+    // the whole tile (at most rowf_stride pairs); used only if that snapshot
+    // describes the current rows
+    if (threadIdx.x == 0 && tma) {
+      if (spec) fence_proxy_async_smem();  // the speculative screen's reads come first
+      mbar_expect_tx(&s_bar, 2u * 16u * (uint32_t)ncopy);
+      tma_bulk_g2s(A0, a.rowf, 16u * (uint32_t)ncopy, &s_bar);
+      tma_bulk_g2s(A1, a.rowf + a.rowf_stride, 16u * (uint32_t)ncopy, &s_bar);
+    }
+    full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
+    // the copies complete on the mbarrier whatever path follows
+    if (tma) mbar_wait(&s_bar, par);
   }
-  const int64_t n = a.n_dev ? (int64_t)*a.n_dev : a.n;
-  const bool compact = a.rowpos && *a.rowpos_n == n;
-
-  bool full_scan = n > tile_rows;  // the host estimate went stale (batches in flight)
-  // the copies complete on the mbarrier whatever path follows
-  if (tma) mbar_wait(&s_bar, 0);
-  if (!full_scan) {
+  if (!spec_ok && !full_scan) {
     const int nr = (int)n;
     double cx = 0.0, cy = 0.0, cz = 0.0;
     float pm = 0.f;
@@ -501,92 +659,11 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
       for (int k = 1; k < kW; ++k) pm = fmaxf(pm, s_pm[k]);
     }
     SF_TL(2);
-    // |p - c| <= sqrt(3) * max_k |P'_k| / (1 - u), rounded up generously
-    const float pmaxf = __fmul_ru(pm, 1.7320508075688774f * (1.0f + 1e-6f));
-
-    // pass 1: lane minima of e
-    float2 fq[kFS][3];
-    float m1[kFS];
-#pragma unroll
-    for (int k = 0; k < kFS; ++k) {
-      const float fx = __double2float_rn(qx[k] - cx), fy = __double2float_rn(qy[k] - cy),
-                  fz = __double2float_rn(qz[k] - cz);
-      fq[k][0] = make_float2(fx, fx);
-      fq[k][1] = make_float2(fy, fy);
-      fq[k][2] = make_float2(fz, fz);
-      m1[k] = INFINITY;
-    }
-    const int np64 = (((nr + 1) / 2) + 63) & ~63;  // padded pairs are +inf
-#pragma unroll 1
-    for (int p = lane; p < np64; p += 64) {
-      const int sa = sf_swz(p), sc = sf_swz(p + 32);
-      const float4 a0 = A0[sa], a1 = A1[sa];
-      const float4 c0 = A0[sc], c1 = A1[sc];
-#pragma unroll
-      for (int k = 0; k < kFS; ++k) {
-        float2 ea = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
-        float2 ec = __ffma2_rn(make_float2(c0.x, c0.y), fq[k][0], make_float2(c1.z, c1.w));
-        ea = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], ea);
-        ec = __ffma2_rn(make_float2(c0.z, c0.w), fq[k][1], ec);
-        ea = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], ea);
-        ec = __ffma2_rn(make_float2(c1.x, c1.y), fq[k][2], ec);
-        m1[k] = fminf(m1[k], fminf(fminf(ea.x, ea.y), fminf(ec.x, ec.y)));
-      }
-    }
+    cnt = sf_screen<kFS>(A0, A1, nr, cx, cy, cz, pm, 0.f, qx, qy, qz, lane, s_cand[warp], s_q[warp],
+                         full_scan);
     SF_TL(3);
-    // screen: every signal's threshold (independent chains, issued together),
-    // then the surviving lanes' units one by one
-    float T[kFS];
-    unsigned tasks[kFS];
-#pragma unroll
-    for (int k = 0; k < kFS; ++k) {
-      float v1 = m1[k], v2 = INFINITY;  // two smallest lane minima
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float o1 = __shfl_xor_sync(0xffffffffu, v1, o);
-        const float o2 = __shfl_xor_sync(0xffffffffu, v2, o);
-        v2 = fminf(fmaxf(v1, o1), fminf(v2, o2));
-        v1 = fminf(v1, o1);
-      }
-      bool ok;
-      T[k] = sf_threshold(v2, pmaxf, qx[k] - cx, qy[k] - cy, qz[k] - cz, ok);
-      full_scan |= !ok;  // warp-uniform
-      tasks[k] = __ballot_sync(0xffffffffu, m1[k] <= T[k]);
-    }
-    int cnt = 0;
-    if (!full_scan) {
-#pragma unroll
-      for (int k = 0; k < kFS; ++k) {
-        unsigned tk = tasks[k];
-        while (tk) {
-          const int l = __ffs(tk) - 1;
-          tk &= tk - 1;
-          for (int i0 = 0; i0 < np64 / 32; i0 += 32) {  // lane l's pairs l + 32 i, one per lane
-            const int p = 32 * (i0 + lane) + l;
-            const bool in = p < np64;
-            const int sp = sf_swz(p);  // conflict-free: lane i reads row i, column l ^ i
-            const float4 a0 = in ? A0[sp] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 a1 = in ? A1[sp] : make_float4(0.f, 0.f, INFINITY, INFINITY);
-            float2 e = __ffma2_rn(make_float2(a0.x, a0.y), fq[k][0], make_float2(a1.z, a1.w));
-            e = __ffma2_rn(make_float2(a0.z, a0.w), fq[k][1], e);
-            e = __ffma2_rn(make_float2(a1.x, a1.y), fq[k][2], e);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const bool pass = in && (h ? e.y : e.x) <= T[k];
-              const unsigned bal = __ballot_sync(0xffffffffu, pass);
-              const int at = cnt + __popc(bal & ((1u << lane) - 1u));
-              if (pass && at < kSfCand) s_cand[warp][at] = ((2 * p + h) << 3) | k;
-              cnt += __popc(bal);
-            }
-          }
-        }
-        if (lane == 0) {
-          s_q[warp][k][0] = qx[k];
-          s_q[warp][k][1] = qy[k];
-          s_q[warp][k][2] = qz[k];
-        }
-      }
-    }
+  }
+  {
     if (!full_scan && cnt <= kSfCand) {
       __syncwarp();
       SF_TL(4);
@@ -603,12 +680,39 @@ __global__ void __launch_bounds__(32 * kW) find_small_f32_kernel(FindArgs a, int
       if (lane < kFS) {
         Best2 b;
         b.init();
+        int c1 = -1, c2 = -1;  // candidate slots of the best two (best2_lex, tracked)
         for (int c = 0; c < cnt; ++c) {
           const int code = s_cand[warp][c];
-          if ((code & 7) == lane) best2_lex(b, s_d[warp][c], code >> 3);
+          if ((code & 7) != lane) continue;
+          const double d = s_d[warp][c];
+          const int32_t i = code >> 3;
+          if (d < b.d1 || (d == b.d1 && i < b.i1)) {
+            b.d2 = b.d1;
+            b.i2 = b.i1;
+            c2 = c1;
+            b.d1 = d;
+            b.i1 = i;
+            c1 = c;
+          } else if (i != b.i1 && (d < b.d2 || (d == b.d2 && i < b.i2))) {
+            b.d2 = d;
+            b.i2 = i;
+            c2 = c;
+          }
         }
         const int64_t j = sig0 + lane;
-        if (j < a.m) write_result(a, j, b);
+        if (j < a.m) {
+          if (spec_ok && a.out_win && !a.out_idx) {  // ids staged with the candidates
+            WinRec w;
+            w.b = c1 >= 0 ? s_cid[warp][c1] : -1;
+            w.s = c2 >= 0 ? s_cid[warp][c2] : -1;
+            w.dwin = __dsqrt_rn(b.d1);  // math.sqrt (correctly rounded): multi.py:72-78
+            a.out_win[j] = w;
+            if (a.firstwin && j < a.fw_limit && w.b >= 0 && w.s >= 0 && w.b != w.s)
+              atomicMin(&a.firstwin[w.b], (int32_t)j);
+          } else {
+            write_result(a, j, b);
+          }
+        }
       }
       sf_store_signals<kFS>(a, sig0, lane, qx, qy, qz);
 #ifdef GS_PROF_TL

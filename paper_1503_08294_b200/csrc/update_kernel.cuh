@@ -975,14 +975,28 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 // row-snapshot hand-off to the next find: each CTA arrives once per launch
 // after its writes the find reads (snapshot rows, counters); the launch's last
 // arrival publishes the batch number (release), see FindArgs::snap_token
-__device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no) {
+// The token is 2 * batch + verdict: verdict 1 tells the next find that its
+// speculative candidates (screened against the other slot, with the bound
+// 2 x that slot's displacement, the find's own rule) stand -- no row changed
+// and no row moved further.
+__device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no,
+                                                bool halted = false) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const int old = atomicAdd(&S.cnt->snap_arrive, 1);
+    Counters* c = S.cnt;
+    const int old = atomicAdd(&c->snap_arrive, 1);
     if ((old + 1) % kCluster == 0) {
       __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token), "r"(batch_no)
+      int verdict = 0;
+      if (!halted) {
+        const int s = S.snap, o = s ^ 1;
+        const float dspec = __fadd_ru(__fmul_ru(2.f, __uint_as_float(c->snap_disp[o])), 1e-30f);
+        verdict = c->snap_gen[s] == c->snap_gen[o] && c->rowpos_n[s] == c->nrows &&
+                  c->rowpos_n[o] == c->nrows && __uint_as_float(c->snap_disp[s]) <= dspec;
+      }
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token),
+                   "r"(2 * batch_no + verdict)
                    : "memory");
     }
   }
@@ -1064,7 +1078,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         if (b >= 0) S.firstwin[b] = kNone32;
       }
     }
-    snapshot_arrive(S, batch_no);
+    snapshot_arrive(S, batch_no, true);
     return;
   }
   const long long t_kernel = clock64();
@@ -1080,7 +1094,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->inserted_start = c->next_id;
     c->stale_n = 0;
     c->nwalk = 0;
-    c->fpm_bits = 0u;
+    c->fpm_bits[S.snap] = 0u;
+    c->snap_disp[S.snap] = 0u;
   }
   // every CTA of the cluster must have started before the first DSMEM
   // exchange; the lead's resets above are read only after later barriers
@@ -1579,10 +1594,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       }
     }
     if (lead) {
-      c->fcen[0] = cx;
-      c->fcen[1] = cy;
-      c->fcen[2] = cz;
+      c->fcen[S.snap][0] = cx;
+      c->fcen[S.snap][1] = cy;
+      c->fcen[S.snap][2] = cz;
+      c->snap_gen[S.snap] = c->row_gen;
     }
+    // the rows' displacement since the other slot's snapshot (same rows only;
+    // the next find's speculative screen checks it against its bound)
+    const bool same_rows = c->snap_gen[S.snap ^ 1] == c->row_gen && c->rowpos_n[S.snap ^ 1] == n;
+    double dmax = same_rows ? 0.0 : INFINITY;
     const int np64 = (((n + 1) / 2) + 63) & ~63;
     float4* A0 = S.rowf;
     float4* A1 = S.rowf + S.rowf_stride;
@@ -1601,6 +1621,12 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           S.rowpos[r] = q.x;
           S.rowpos[U + r] = q.y;
           S.rowpos[2 * U + r] = q.z;
+          if (same_rows) {
+            const double dx = q.x - S.rowpos_prev[r], dy = q.y - S.rowpos_prev[U + r],
+                         dz = q.z - S.rowpos_prev[2 * U + r];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 == d2) dmax = fmax(dmax, d2);  // (dead rows: inf - inf)
+          }
           if (isfinite(q.x) && isfinite(q.y) && isfinite(q.z)) {
             const float px = __double2float_rn(q.x - cx), py = __double2float_rn(q.y - cy),
                         pz = __double2float_rn(q.z - cz);
@@ -1618,7 +1644,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) pm = fmaxf(pm, __shfl_xor_sync(0xffffffffu, pm, o));
-    if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits, __float_as_uint(pm));
+    if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits[S.snap], __float_as_uint(pm));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if ((tid & 31) == 0 && dmax > 0.0) {  // sqrt, rounded up with room for the FP64 rounding
+      const float db = __double2float_ru(sqrt(dmax) * (1.0 + 1e-9));
+      atomicMax(&c->snap_disp[S.snap], __float_as_uint(db));
+    }
   }
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
@@ -1628,10 +1660,10 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     next_minla(S, batch_no, g);
     return;
   }
-  if (tid == 0) c->rowpos_n = c->nrows;
+  if (tid == 0) c->rowpos_n[S.snap] = c->nrows;
   // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
   if (c->ndead_rows * 8 > c->nrows) {
-    if (tid == 0) c->rowpos_n = -1;  // the rows move: the next find gathers
+    if (tid == 0) c->rowpos_n[S.snap] = -1;  // the rows move: the next find gathers
     const int n = c->nrows;
     int out = 0;
     for (int base = 0; base < n; base += kUpdThreads) {
@@ -1646,6 +1678,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     }
     if (tid == 0) {
       c->nrows = out;
+      c->row_gen++;
       c->ndead_rows = 0;
     }
   }
