@@ -117,7 +117,10 @@ struct Counters {
   // its part of the snapshot (monotone count); the last one publishes the
   // launch's batch number in S.snap_token, on which the next find starts
   // (before the update grid has drained)
-  int snap_arrive;
+  // low 32 bits: CTA arrivals (a multiple of the cluster size between
+  // launches), high 32: arrivals whose part broke the speculative verdict
+  // (reset by each launch's lead)
+  unsigned long long snap_word;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
   // FP32 unit pairs of the row snapshot (the screened find's staging): centre

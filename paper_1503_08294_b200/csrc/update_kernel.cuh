@@ -979,24 +979,20 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 // speculative candidates (screened against the other slot, with the bound
 // 2 x that slot's displacement, the find's own rule) stand -- no row changed
 // and no row moved further.
-__device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no,
-                                                bool halted = false) {
+// Each CTA's part of the verdict travels with its arrival (the count of
+// failing parts in the arrival word's high half), so the last arrival
+// publishes without reading anything else.
+__device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no, bool part_ok) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    Counters* c = S.cnt;
-    const int old = atomicAdd(&c->snap_arrive, 1);
-    if ((old + 1) % kCluster == 0) {
+    const unsigned long long inc = 1ull + ((unsigned long long)(part_ok ? 0u : 1u) << 32);
+    const unsigned long long old = atomicAdd(&S.cnt->snap_word, inc);
+    if (((unsigned)old + 1u) % kCluster == 0) {
+      const unsigned fails = (unsigned)(old >> 32) + (part_ok ? 0u : 1u);
       __threadfence();
-      int verdict = 0;
-      if (!halted) {
-        const int s = S.snap, o = s ^ 1;
-        const float dspec = __fadd_ru(__fmul_ru(2.f, __uint_as_float(c->snap_disp[o])), 1e-30f);
-        verdict = c->snap_gen[s] == c->snap_gen[o] && c->rowpos_n[s] == c->nrows &&
-                  c->rowpos_n[o] == c->nrows && __uint_as_float(c->snap_disp[s]) <= dspec;
-      }
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token),
-                   "r"(2 * batch_no + verdict)
+                   "r"(2 * batch_no + (fails == 0u ? 1 : 0))
                    : "memory");
     }
   }
@@ -1042,6 +1038,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
   __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
+  __shared__ bool s_dok[kUpdThreads / 32];  // the snapshot part's displacement within the bound
   __shared__ int s_defer_sm[kDeferSm];  // deferred ring recomputes (event path)
   __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
   // this CTA's processed signals of the window, compacted in batch order:
@@ -1078,7 +1075,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         if (b >= 0) S.firstwin[b] = kNone32;
       }
     }
-    snapshot_arrive(S, batch_no, true);
+    snapshot_arrive(S, batch_no, false);  // (no snapshot: no verdict)
     return;
   }
   const long long t_kernel = clock64();
@@ -1096,6 +1093,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->nwalk = 0;
     c->fpm_bits[S.snap] = 0u;
     c->snap_disp[S.snap] = 0u;
+    c->snap_word = 0ull;  // (a multiple of the cluster size: the arrival count restarts)
   }
   // every CTA of the cluster must have started before the first DSMEM
   // exchange; the lead's resets above are read only after later barriers
@@ -1603,6 +1601,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // the next find's speculative screen checks it against its bound)
     const bool same_rows = c->snap_gen[S.snap ^ 1] == c->row_gen && c->rowpos_n[S.snap ^ 1] == n;
     double dmax = same_rows ? 0.0 : INFINITY;
+    // the next find's bound (its rule: 2 x the previous update's displacement)
+    const float dspec_part = __fadd_ru(__fmul_ru(2.f, __uint_as_float(c->snap_disp[S.snap ^ 1])), 1e-30f);
     const int np64 = (((n + 1) / 2) + 63) & ~63;
     float4* A0 = S.rowf;
     float4* A1 = S.rowf + S.rowf_stride;
@@ -1647,16 +1647,22 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     if ((tid & 31) == 0 && pm > 0.f) atomicMax(&c->fpm_bits[S.snap], __float_as_uint(pm));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    if ((tid & 31) == 0 && dmax > 0.0) {  // sqrt, rounded up with room for the FP64 rounding
-      const float db = __double2float_ru(sqrt(dmax) * (1.0 + 1e-9));
-      atomicMax(&c->snap_disp[S.snap], __float_as_uint(db));
+    float db = 0.f;
+    if (dmax > 0.0) db = __double2float_ru(sqrt(dmax) * (1.0 + 1e-9));  // rounded up, FP64 room
+    if ((tid & 31) == 0) {
+      if (db > 0.f) atomicMax(&c->snap_disp[S.snap], __float_as_uint(db));
+      s_dok[tid >> 5] = db <= dspec_part;
     }
   }
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
 #endif
+  __syncthreads();
+  bool part_ok = true;
+#pragma unroll
+  for (int q = 0; q < kUpdThreads / 32; ++q) part_ok = part_ok && s_dok[q];
   if (crank != 0) {
-    snapshot_arrive(S, batch_no);
+    snapshot_arrive(S, batch_no, part_ok);
     next_minla(S, batch_no, g);
     return;
   }
@@ -1682,7 +1688,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       c->ndead_rows = 0;
     }
   }
-  snapshot_arrive(S, batch_no);  // (includes the block barrier)
+  // (a compaction moves the rows: the candidates of the other slot are void)
+  snapshot_arrive(S, batch_no, part_ok && c->rowpos_n[S.snap] >= 0);
   next_minla(S, batch_no, g);
 #if GS_PROF_TAIL
   if (tid == 0) {
