@@ -286,13 +286,9 @@ __device__ long long block_min_ll(long long v, long long* s_ll32) {
 // and counts its induced degree against N(u) staged in shared memory; the
 // connectivity test expands a bitmask frontier with warp OR-reductions.
 // All 32 lanes must call it with the same u.
-__device__ int classify_ring_warp(const DevState& S, int u, int* sh) {
+// (k, v: u's degree and slot `lane` of its row, loaded by the caller)
+__device__ int classify_ring_warp(const DevState& S, int u, int* sh, int k, int v) {
   const int lane = threadIdx.x & 31;
-  // two dependent levels (u's row, then every neighbour's row), each issued
-  // speculatively together with the degree it is masked by
-  const int2* A = S.adj + (size_t)u * kMaxDeg;
-  const int k = S.deg[u];
-  const int v = A[lane].x;  // slots past deg(u) are ignored below
   if (k < 2) return kRingInc;
   if (k > 32) return classify_ring(S, u);
   if (lane < k) sh[lane] = v;
@@ -1497,10 +1493,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
           for (int q0 = 0; q0 < i; q0 += 32)
             dup |= q0 + lane < i && defer_at(S, s_defer_sm, q0 + lane) == u;
           if (__any_sync(0xffffffffu, dup)) continue;
-          if (S.alive[u]) {
-            const int nw = classify_ring_warp(S, u, s_ring_sh[warp]);
+          // one load level for the unit's state and row (slots past the degree
+          // are ignored); the neighbours' rows are the second
+          const uint8_t alive_u = S.alive[u];
+          const int old = S.ring[u];
+          const int ku = S.deg[u];
+          const int vu = S.adj[(size_t)u * kMaxDeg + lane].x;
+          if (alive_u) {
+            const int nw = classify_ring_warp(S, u, s_ring_sh[warp], ku, vu);
             if (lane == 0) {
-              const int old = S.ring[u];
               if (nw != old) {
                 S.ring[u] = (uint8_t)nw;
                 atomicAdd(&c->ring_counts[old], -1);
