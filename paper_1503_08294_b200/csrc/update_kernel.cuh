@@ -902,10 +902,6 @@ __device__ __forceinline__ int crank_of() {
   }
 }
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
-#ifndef GS_LOOK_MIN
-#define GS_LOOK_MIN 64
-#endif
-constexpr int kLookMin = GS_LOOK_MIN;  // resumed segments' minimum lookahead (ranks)
 
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
 // used with alternating parity so a CTA running one call ahead cannot
@@ -1108,13 +1104,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   // and the next one starts at j*+1.
   bool resume = false;
   int rbase = 0, nproc = 0, wend = 0;
-  // event-dense windows: a resumed segment evaluates only the next rlim -
-  // rbase ranks (4x the ranks per event so far in the window, at least
-  // kLookMin); without an event among them it stops before rank rlim (a
-  // "pseudo event": the segment commits, no event runs) and the next one
-  // resumes there.  B's work -- the bound of an event-dense segment --
-  // shrinks with it; a sparse window keeps one unlimited segment.
-  int ev_win = 0, rlim = 0;
   long long tick0 = 0, minla = 0;
   bool cand = false;
   int cb = -1;
@@ -1231,16 +1220,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #if GS_PROF_B
     const long long tb0 = clock64();
 #endif
-    if (!resume) {
-      ev_win = 0;
-      rlim = nproc;
-    } else {
-      const int look = max(kLookMin, 4 * (rbase / max(ev_win, 1)));
-      rlim = (int)min((long long)nproc, (long long)rbase + look);
-    }
-    if (p_valid && p_rank == rlim && rlim < nproc)  // the pseudo event
-      evkey = ((long long)p_rank << 32) | (unsigned)p_j;
-    if (p_valid && p_rank >= rbase && p_rank < rlim) {
+    if (p_valid && p_rank >= rbase) {
       const int r = p_rank;
       const int jj = p_j;
       const int b = p_b, s = p_s;
@@ -1324,7 +1304,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     const bool has_ev = kmin != 0x7fffffffffffffffLL;
     const int rstar = has_ev ? (int)(kmin >> 32) : nproc;
     const int jstar = has_ev ? (int)(kmin & 0xffffffffLL) : wend;
-    const bool pseudo = has_ev && rstar == rlim;  // no event before the lookahead's end
     if (lead) { const long long t_ = clock64(); acc[2] += t_ - t_ph; t_ph = t_; }
 #if GS_PROF_B
     if (lead) {
@@ -1407,16 +1386,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     //      deferred rings, the lead thread finishes (sweep, adapt_threshold);
     //      one cluster barrier publishes the result (two more only when a
     //      sweep must scan for stale units)
-    if (pseudo) {
-      // the committed ranks' stores (firstwin clears included) are published
-      // and the segment resumes at the first rank not evaluated
-      csync();
-      resume = true;
-      rbase = rstar;
-      continue;
-    }
     if (rstar < nproc) {
-      ++ev_win;
       const long long t_ser = clock64();
       if (crank == 0) {
         if (tid == 0) s_defer_n = 0;
