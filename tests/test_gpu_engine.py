@@ -294,3 +294,24 @@ def test_run_multi_device_sampling_matches_golden(name):
         assert int(getattr(st, k)) == int(gold[f"stat_{k}"]), k
     assert_state_equal(net.export(), gold)
     net.audit()
+
+
+@pytest.mark.parametrize("spec", ["0", "1"])
+@pytest.mark.parametrize("name", ["cfg1", "v8k_fixed"])
+def test_speculative_screen_on_and_off_match_golden(name, spec, monkeypatch):
+    """The find's speculative screen (against the snapshot before the running
+    update, threshold widened by a movement bound, verdict from the update's
+    token) and the plain screen give the reference's run bit for bit; the
+    engine reads GS_SPEC_FIND when it is created."""
+    from paper_1503_08294_b200 import EngineParams, run_multi
+
+    monkeypatch.setenv("GS_SPEC_FIND", spec)
+    gold = load_golden(name)
+    if not same_numpy(gold):
+        pytest.skip("golden made with another numpy")
+    case = CASES[name]
+    params = EngineParams(**case["params"])
+    net, st = run_multi(make_source(case["source"]), params, case["seed"])
+    for k in ("iterations", "signals", "units", "connections", "converged"):
+        assert int(getattr(st, k)) == int(gold[f"stat_{k}"]), k
+    assert_state_equal(net.export(), gold)
