@@ -1568,7 +1568,47 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   const long long tt0 = clock64();
 #endif
   if (start_wait) cwait();  // (no window ran: m == 0)
+  if (lead) {  // the lead's phase timers (the stats thread reads them after the barrier)
+#pragma unroll
+    for (int q = 0; q < 12; ++q)
+      if (acc[q]) atomicAdd((unsigned long long*)&c->cyc_phase[q], (unsigned long long)acc[q]);
+    atomicAdd((unsigned long long*)&c->cyc_serial, (unsigned long long)acc[12]);
+    atomicAdd((unsigned long long*)&c->cyc_total, (unsigned long long)(clock64() - t_kernel));
+  }
   csync();  // the last window's walk stores are visible to the snapshot below
+  if (g == kWinC - 1) {
+    // the batch's stats, on a thread without a share of the row snapshot
+    // (unless the rows fill every thread): off the hand-off's path and done
+    // by the time a short next find waits for this grid.  is_converged:
+    // engine.py:358-365 (max(h) < h_t <=> no untrained unit)
+    const int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
+    c->converged = (c->n_units >= 4 && ok == c->n_units && c->untrained == 0) ? 1 : 0;
+    c->batches++;
+    if (c->converged && c->halt_on_converge) c->halted = 1;
+    gs_batch_stats* st = S.stats;
+    st->processed = c->processed;
+    st->discarded = c->discarded;
+    st->inserted = c->next_id - c->inserted_start;
+    st->units = c->n_units;
+    st->edges = c->n_edges;
+    st->next_id = c->next_id;
+    st->converged = c->converged;
+    st->tick = c->tick;
+    st->events = c->events;
+    st->windows = c->windows;
+    st->error = c->error;
+    st->max_degree = c->max_degree;
+    st->ev_create = c->ev_create;
+    st->ev_insert = c->ev_insert;
+    st->ev_prune = c->ev_prune;
+    st->ev_sweep = c->ev_sweep;
+    st->cyc_serial = c->cyc_serial;
+    st->cyc_total = c->cyc_total;
+    st->batches = c->batches;
+    st->halted = c->halted;
+    for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
+    if (st_out != st) *st_out = *st;  // the batch's device ring slot
+  }
 #if GS_PROF_TAIL
   const long long tt1 = clock64();
 #endif
@@ -1693,65 +1733,21 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   snapshot_arrive(S, batch_no, part_ok && c->rowpos_n[S.snap] >= 0);
   next_minla(S, batch_no, g);
 #if GS_PROF_TAIL
-  if (tid == 0) {
+  if (tid == 0) {  // (reach the stats one batch late)
     const long long tt3 = clock64();
-    acc[3] += tt1 - tt0;   // tail: barrier
-    acc[10] += tt2 - tt1;  // tail: row snapshot
-    acc[11] += tt3 - tt2;  // tail: compaction check
+    atomicAdd((unsigned long long*)&c->cyc_phase[3], (unsigned long long)(tt1 - tt0));
+    atomicAdd((unsigned long long*)&c->cyc_phase[10], (unsigned long long)(tt2 - tt1));
+    atomicAdd((unsigned long long*)&c->cyc_phase[11], (unsigned long long)(tt3 - tt2));
   }
 #endif
-  if (tid == 0) {
-    // is_converged: engine.py:358-365 (max(h) < h_t <=> no untrained unit)
-    const int ok = c->ring_counts[kRingDisk] + (P.allow_boundary ? c->ring_counts[kRingHalf] : 0);
-    c->converged = (c->n_units >= 4 && ok == c->n_units && c->untrained == 0) ? 1 : 0;
-    c->batches++;
-    if (c->converged && c->halt_on_converge) c->halted = 1;
-    gs_batch_stats* st = S.stats;
-    st->processed = c->processed;
-    st->discarded = c->discarded;
-    st->inserted = c->next_id - c->inserted_start;
-    st->units = c->n_units;
-    st->edges = c->n_edges;
-    st->next_id = c->next_id;
-    st->converged = c->converged;
-    st->tick = c->tick;
-    st->events = c->events;
-    st->windows = c->windows;
-    st->error = c->error;
-    st->max_degree = c->max_degree;
-    st->ev_create = c->ev_create;
-    st->ev_insert = c->ev_insert;
-    st->ev_prune = c->ev_prune;
-    st->ev_sweep = c->ev_sweep;
-    c->cyc_total += clock64() - t_kernel;
-#pragma unroll
-    for (int q = 0; q < 12; ++q) c->cyc_phase[q] += acc[q];
-    c->cyc_serial += acc[12];
-    st->cyc_serial = c->cyc_serial;
-    st->cyc_total = c->cyc_total;
-    st->batches = c->batches;
-    st->halted = c->halted;
-    for (int q = 0; q < 12; ++q) st->cyc_phase[q] = c->cyc_phase[q];
 #ifdef GS_PROF_TL
-    {
-      unsigned long long tl2;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
-      unsigned long long* g = g_tlu[batch_no & 8191];
-      g[0] = tl0;
-      g[1] = tl1;
-      g[2] = tl2;
-    }
-#endif
-    // the host's ring slot (pinned, mapped): no copy between the kernels
-#ifndef GS_NO_HOST_STATS
-    if (st_out != st) {
-#else
-    if (false) {
-#endif
-      *st_out = *st;
-#if GS_STATS_FENCE
-      __threadfence_system();  // (the host reads the slot only after an event)
-#endif
-    }
+  if (tid == 0) {
+    unsigned long long tl2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tl2));
+    unsigned long long* gt = g_tlu[batch_no & 8191];
+    gt[0] = tl0;
+    gt[1] = tl1;
+    gt[2] = tl2;
   }
+#endif
 }

@@ -1,7 +1,7 @@
 """Per-batch critical path of the find -> update chain from a timeline
 profiling build (-DGS_PROF_TL=0: globaltimer stamps kept on the device, no
 printing): one config-3 run through run_multi, then the stamps.
-Usage: GS_LIB_PATH=<tl build> python tools/tl_gaps.py [batches]"""
+Usage: GS_LIB_PATH=<tl build> python tools/tl_gaps.py [batches] [workload]"""
 import ctypes as C
 import os
 import sys
@@ -13,7 +13,8 @@ from paper_1503_08294_b200 import _lib, workloads  # noqa: E402
 from paper_1503_08294_b200.multi import run_multi  # noqa: E402
 
 nb = int(sys.argv[1]) if len(sys.argv) > 1 else 8000
-src, params, seed, _ = workloads.make("cfg3")
+NAME = sys.argv[2] if len(sys.argv) > 2 else "cfg3"
+src, params, seed, _ = workloads.make(NAME)
 params = type(params)(**{**params.__dict__, "max_signals": nb * params.batch_cap})
 net, st = run_multi(src, params, seed, capacity=8192)
 n = min(st.iterations + 1, 8192)
