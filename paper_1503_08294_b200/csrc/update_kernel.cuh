@@ -996,11 +996,13 @@ __device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no,
 
 // the next batch's silent-sweep value: minimum last_active over live units
 // (after the snapshot hand-off: only the next update reads it)
-__device__ __forceinline__ void next_minla(const DevState& S, int batch_no, int g) {
-  Counters* c = S.cnt;
-  long long mla = 0x7fffffffffffffffLL;
-  const int nid_e = c->next_id;
-  for (int u = g; u < nid_e; u += kWinC) {
+// (the loads and the warp's minimum before the hand-off, with the snapshot's;
+// the fire-and-forget atomic after it)
+// (la0 / al0: unit g's last_active and liveness, loaded with the snapshot)
+__device__ __forceinline__ long long minla_part(const DevState& S, int g, long long la0, bool al0) {
+  long long mla = (la0 != -1 && al0) ? la0 : 0x7fffffffffffffffLL;
+  const int nid_e = S.cnt->next_id;
+  for (int u = g + kWinC; u < nid_e; u += kWinC) {
     const long long t = S.la_val[u];
     if (t != -1 && S.alive[u] && t < mla) mla = t;
   }
@@ -1009,8 +1011,11 @@ __device__ __forceinline__ void next_minla(const DevState& S, int batch_no, int 
     const long long t = __shfl_xor_sync(0xffffffffu, mla, o);
     mla = t < mla ? t : mla;
   }
+  return mla;
+}
+__device__ __forceinline__ void next_minla(const DevState& S, int batch_no, long long mla) {
   if ((threadIdx.x & 31) == 0 && mla != 0x7fffffffffffffffLL)
-    atomicMin(&c->minla_next[(batch_no + 1) & 1], mla);
+    atomicMin(&S.cnt->minla_next[(batch_no + 1) & 1], mla);
 }
 
 // ---------------------------------------------------------------------------
@@ -1576,6 +1581,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     atomicAdd((unsigned long long*)&c->cyc_total, (unsigned long long)(clock64() - t_kernel));
   }
   csync();  // the last window's walk stores are visible to the snapshot below
+  // unit g's last_active / liveness for the next batch's silent-sweep value,
+  // loaded with the snapshot's loads (reduced after it)
+  long long la_g = -1;
+  bool al_g = false;
+  if (g < c->next_id) {
+    la_g = S.la_val[g];
+    al_g = S.alive[g] != 0;
+  }
   if (g == kWinC - 1) {
     // the batch's stats, on a thread without a share of the row snapshot
     // (unless the rows fill every thread): off the hand-off's path and done
@@ -1698,13 +1711,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
 #if GS_PROF_TAIL
   const long long tt2 = clock64();
 #endif
+  const long long mla_w = minla_part(S, g, la_g, al_g);
   __syncthreads();
   bool part_ok = true;
 #pragma unroll
   for (int q = 0; q < kUpdThreads / 32; ++q) part_ok = part_ok && s_dok[q];
   if (crank != 0) {
     snapshot_arrive(S, batch_no, part_ok);
-    next_minla(S, batch_no, g);
+    next_minla(S, batch_no, mla_w);
     return;
   }
   if (tid == 0) c->rowpos_n[S.snap] = c->nrows;
@@ -1731,7 +1745,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   }
   // (a compaction moves the rows: the candidates of the other slot are void)
   snapshot_arrive(S, batch_no, part_ok && c->rowpos_n[S.snap] >= 0);
-  next_minla(S, batch_no, g);
+  next_minla(S, batch_no, mla_w);
 #if GS_PROF_TAIL
   if (tid == 0) {  // (reach the stats one batch late)
     const long long tt3 = clock64();
