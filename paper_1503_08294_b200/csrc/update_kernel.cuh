@@ -1081,11 +1081,11 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   }
   const long long t_kernel = clock64();
   long long t_ph = t_kernel;
-  // the lead thread's phase timers stay in registers until the kernel ends
-  // (a global read-modify-write per phase would sit on its critical path)
-  long long acc[13];
-#pragma unroll
-  for (int q = 0; q < 13; ++q) acc[q] = 0;
+  // the lead thread's phase timers in shared memory until the kernel ends (a
+  // global read-modify-write per phase would sit on its critical path, and
+  // registers for them in every thread would add to the kernel's spills)
+  __shared__ long long acc[13];
+  if (tid < 13) acc[tid] = 0;
   if (lead) {
     c->minla_next[(batch_no + 1) & 1] = 0x7fffffffffffffffLL;  // the tail's atomicMin target
     c->processed = c->discarded = c->events = c->windows = 0;
