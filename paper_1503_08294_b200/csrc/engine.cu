@@ -1166,12 +1166,15 @@ long long run_op(gs_engine* e, const OpArgs& a, long long* res2 = nullptr) {
 
 void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64_t m,
                    gs_batch_stats* st_out = nullptr, bool pre_fw = false) {
-  if constexpr (kCluster > 8) {  // clusters beyond the portable 8 CTAs need an opt-in
-    static bool opted = false;
-    if (!opted) {
+  static bool opted = false;
+  if (!opted) {
+    // clusters beyond the portable 8 CTAs need an opt-in; C1's staging in
+    // shared memory is more than the default 48 KB
+    if constexpr (kCluster > 8)
       GS_CUDA(cudaFuncSetAttribute(k_update_batch, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      opted = true;
-    }
+    GS_CUDA(cudaFuncSetAttribute(k_update_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kUpdDynSmem));
+    opted = true;
   }
   e->batch_no++;
   {  // this update's row-snapshot slot
@@ -1184,6 +1187,7 @@ void launch_update(gs_engine* e, const double* d_sig, const WinRec* d_rec, int64
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCluster);
   cfg.blockDim = dim3(kUpdThreads);
+  cfg.dynamicSmemBytes = kUpdDynSmem;
   cfg.stream = e->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -902,6 +902,8 @@ __device__ __forceinline__ int crank_of() {
   }
 }
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
+// dynamic shared memory of the update kernel: B's per-rank results for C1
+constexpr int kUpdDynSmem = (int)((sizeof(int2) + 2 * sizeof(int)) * 2 * kStage * kUpdThreads);
 
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
 // used with alternating parity so a CTA running one call ahead cannot
@@ -1039,6 +1041,13 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
   __shared__ int s_ring_sh[32][33];  // per-warp N(u) staging for classify_ring_warp
   __shared__ int s_stage[kMaxDeg];    // event warp: adjacency staging
   __shared__ int s_defer_n;
+  // B's per-rank results for C1 ([entry][thread]: conflict-free), 64 KB
+  extern __shared__ __align__(16) unsigned char s_c1dyn[];
+  int2 (*s_c1nb)[kUpdThreads] = reinterpret_cast<int2 (*)[kUpdThreads]>(s_c1dyn);
+  int (*s_c1a)[kUpdThreads] =
+      reinterpret_cast<int (*)[kUpdThreads]>(s_c1dyn + sizeof(int2) * 2 * kStage * kUpdThreads);
+  int (*s_c1j)[kUpdThreads] = reinterpret_cast<int (*)[kUpdThreads]>(
+      s_c1dyn + (sizeof(int2) + sizeof(int)) * 2 * kStage * kUpdThreads);
   __shared__ bool s_dok[kUpdThreads / 32];  // the snapshot part's displacement within the bound
   __shared__ int s_defer_sm[kDeferSm];  // deferred ring recomputes (event path)
   __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
@@ -1276,6 +1285,17 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       // segment-start state (networks above kWinC units only)
       if (nid_b > nwalked && !ev && hb_low && !adapt_ring_ok(P, ringb))
         c1_far = far_nbrs_trained(S, P, jj, db, c1_nb0, c1_nb1, nwalked);
+      // C1's inputs wait in shared memory (not in registers across the walk
+      // and the reduction: the kernel is at its register limit)
+#pragma unroll
+      for (int k = 0; k < kStage; ++k) {
+        s_c1nb[k][tid] = c1_nb0[k];
+        s_c1nb[kStage + k][tid] = c1_nb1[k];
+        s_c1a[k][tid] = c1_a0[k];
+        s_c1a[kStage + k][tid] = c1_a1[k];
+        s_c1j[k][tid] = c1_j0[k];
+        s_c1j[kStage + k][tid] = c1_j1[k];
+      }
     }
     // this thread's unit slot replayed as if the whole window commits
     double4 wk_p;
@@ -1323,6 +1343,15 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     const bool com = p_valid && p_rank >= rbase && p_rank < rstar;
     int cb_com = -1;
     if (com) {
+#pragma unroll
+      for (int k = 0; k < kStage; ++k) {
+        c1_nb0[k] = s_c1nb[k][tid];
+        c1_nb1[k] = s_c1nb[kStage + k][tid];
+        c1_a0[k] = s_c1a[k][tid];
+        c1_a1[k] = s_c1a[kStage + k][tid];
+        c1_j0[k] = s_c1j[k][tid];
+        c1_j1[k] = s_c1j[kStage + k][tid];
+      }
       const int cj = p_j;
       const int cb = p_b;
       cb_com = cb;
