@@ -902,8 +902,10 @@ __device__ __forceinline__ int crank_of() {
   }
 }
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
-// dynamic shared memory of the update kernel: B's per-rank results for C1
-constexpr int kUpdDynSmem = (int)((sizeof(int2) + 2 * sizeof(int)) * 2 * kStage * kUpdThreads);
+// dynamic shared memory of the update kernel: B's per-rank results for C1,
+// the walk's replay result
+constexpr int kC1Smem = (int)((sizeof(int2) + 2 * sizeof(int)) * 2 * kStage * kUpdThreads);
+constexpr int kUpdDynSmem = kC1Smem + (int)((sizeof(double4) + sizeof(double2)) * kUpdThreads);
 
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
 // used with alternating parity so a CTA running one call ahead cannot
@@ -1048,6 +1050,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       reinterpret_cast<int (*)[kUpdThreads]>(s_c1dyn + sizeof(int2) * 2 * kStage * kUpdThreads);
   int (*s_c1j)[kUpdThreads] = reinterpret_cast<int (*)[kUpdThreads]>(
       s_c1dyn + (sizeof(int2) + sizeof(int)) * 2 * kStage * kUpdThreads);
+  // the walk's replay result (position; habituation after / before)
+  double4* s_wk = reinterpret_cast<double4*>(s_c1dyn + kC1Smem);
+  double2* s_wkh = reinterpret_cast<double2*>(s_c1dyn + kC1Smem + sizeof(double4) * kUpdThreads);
   __shared__ bool s_dok[kUpdThreads / 32];  // the snapshot part's displacement within the bound
   __shared__ int s_defer_sm[kDeferSm];  // deferred ring recomputes (event path)
   __shared__ __align__(16) Counters s_cnt;  // event warp's working copy of the counters
@@ -1298,14 +1303,18 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       }
     }
     // this thread's unit slot replayed as if the whole window commits
-    double4 wk_p;
-    double wk_h = 0.0, wk_h0 = 0.0;
     int wk_max = -1;
     if (u_w >= 0 && u_w < nid_b) {
-      wk_h0 = S.hab[u_w];
+      double4 wk_p;
+      double wk_h;
+      const double wk_h0 = S.hab[u_w];
       int tt;
       wk_max = walk_compute(S, P, sig, u_w, wend, wk_p, wk_h, tt);
       S.ttr[u_w] = tt;  // read by C1's adapt_threshold after the barrier below
+      // the replay waits in shared memory across the reduction (registers
+      // are the kernel's limit)
+      s_wk[tid] = wk_p;
+      s_wkh[tid] = make_double2(wk_h, wk_h0);
     }
 #if GS_PROF_B
     {  // the slowest thread's B / walk work before the reduction (cycles)
@@ -1381,7 +1390,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     //      at or after the event (then this slot is replayed again)
     const bool fast = !has_ev && nid_b <= nwalked;
     if (wk_max >= 0) {
-      if (wk_max < jstar) walk_store(S, P, u_w, wk_p, wk_h, wk_h0);
+      if (wk_max < jstar) walk_store(S, P, u_w, s_wk[tid], s_wkh[tid].x, s_wkh[tid].y);
       else walk_unit(S, P, sig, u_w, jstar);
     }
     for (int u = nwalked + g; u < nid_b; u += kWinC) walk_unit(S, P, sig, u, jstar);
