@@ -904,7 +904,8 @@ __device__ __forceinline__ int crank_of() {
 constexpr int kWinC = kCluster * kUpdThreads;  // one window signal per thread
 // dynamic shared memory of the update kernel: B's per-rank results for C1,
 // the walk's replay result
-constexpr int kC1Smem = (int)((sizeof(int2) + 2 * sizeof(int)) * 2 * kStage * kUpdThreads);
+constexpr int kC1Smem = (int)((sizeof(int2) + 2 * sizeof(int)) * 2 * kStage * kUpdThreads +
+                              sizeof(int) * kUpdThreads);
 constexpr int kUpdDynSmem = kC1Smem + (int)((sizeof(double4) + sizeof(double2)) * kUpdThreads);
 
 // exclusive scan over the whole cluster; s_cta is a [2][kCluster] buffer
@@ -1050,6 +1051,7 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
       reinterpret_cast<int (*)[kUpdThreads]>(s_c1dyn + sizeof(int2) * 2 * kStage * kUpdThreads);
   int (*s_c1j)[kUpdThreads] = reinterpret_cast<int (*)[kUpdThreads]>(
       s_c1dyn + (sizeof(int2) + sizeof(int)) * 2 * kStage * kUpdThreads);
+  int* s_c1s = s_c1j[2 * kStage];  // C1's packed scalars (one int per thread)
   // the walk's replay result (position; habituation after / before)
   double4* s_wk = reinterpret_cast<double4*>(s_c1dyn + kC1Smem);
   double2* s_wkh = reinterpret_cast<double2*>(s_c1dyn + kC1Smem + sizeof(double4) * kUpdThreads);
@@ -1292,6 +1294,8 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         c1_far = far_nbrs_trained(S, P, jj, db, c1_nb0, c1_nb1, nwalked);
       // C1's inputs wait in shared memory (not in registers across the walk
       // and the reduction: the kernel is at its register limit)
+      // (ring 2 bits, hb_low, far, degree 6 bits, patience the rest)
+      s_c1s[tid] = c1_ring | (c1_hblow ? 4 : 0) | (c1_far ? 8 : 0) | (c1_d << 4) | (c1_patb << 10);
 #pragma unroll
       for (int k = 0; k < kStage; ++k) {
         s_c1nb[k][tid] = c1_nb0[k];
@@ -1352,6 +1356,14 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     const bool com = p_valid && p_rank >= rbase && p_rank < rstar;
     int cb_com = -1;
     if (com) {
+      {
+        const int w = s_c1s[tid];
+        c1_ring = w & 3;
+        c1_hblow = (w & 4) != 0;
+        c1_far = (w & 8) != 0;
+        c1_d = (w >> 4) & 63;
+        c1_patb = w >> 10;
+      }
 #pragma unroll
       for (int k = 0; k < kStage; ++k) {
         c1_nb0[k] = s_c1nb[k][tid];
