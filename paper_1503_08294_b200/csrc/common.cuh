@@ -260,11 +260,13 @@ struct FindArgs {
   // first window then starts with its candidates resolved
   int32_t* firstwin = nullptr;
   int64_t fw_limit = 0;
-  // non-null: the preceding update publishes snap_target here once its row
-  // snapshot is complete (the screened find starts on it, not on the grid's
-  // completion; it still waits for that before it exits)
+  // non-null: each of the preceding update's snap_parts CTAs stores
+  // 2 * snap_target + verdict in snap_token[part] once its part of the row
+  // snapshot is complete (the screened find starts on them, not on the
+  // grid's completion; it still waits for that before it exits)
   const int* snap_token = nullptr;
   int snap_target = 0;
+  int snap_parts = 0;
   // speculative screen (the screened find, engine batches): the snapshot
   // before the preceding update (its FP32 pairs, centre, max-norm, rows) and
   // the row generations / largest displacements of both snapshots

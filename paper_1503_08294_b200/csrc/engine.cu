@@ -113,14 +113,8 @@ struct Counters {
   // written): the silent-sweep test's value for a first window the find
   // resolved
   long long minla_next[2];
-  // row snapshot hand-off: every update CTA arrives once per launch after
-  // its part of the snapshot (monotone count); the last one publishes the
-  // launch's batch number in S.snap_token, on which the next find starts
-  // (before the update grid has drained)
-  // low 32 bits: CTA arrivals (a multiple of the cluster size between
-  // launches), high 32: arrivals whose part broke the speculative verdict
-  // (reset by each launch's lead)
-  unsigned long long snap_word;
+  // (row snapshot hand-off: S.snap_token, one flag per update CTA)
+  unsigned long long snap_word_unused;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
   // FP32 unit pairs of the row snapshot (the screened find's staging): centre
@@ -171,7 +165,12 @@ struct DevState {
   int* defer_sm;        // the event path's shared-memory part of the deferred list
   Counters* cnt;
   gs_batch_stats* stats;
-  int* snap_token;  // own 128-byte line: the next find's CTAs poll it
+  // row snapshot hand-off, own 128-byte line: update CTA q stores
+  // 2 * batch + (its part keeps the speculative verdict) in snap_token[q]
+  // once its part of the snapshot is written; the next find's CTAs poll the
+  // kCluster flags and start when all carry the batch (before the update
+  // grid has drained) -- no atomics, no reset, a halted launch stores too
+  int* snap_token;
   int U, EC;
   int rowf_stride;  // unit pairs per half of rowf (multiple of 64)
 };
@@ -1237,6 +1236,7 @@ void launch_find(gs_engine* e, const double* d_sig, int64_t lo, int64_t hi, WinR
     if (e->batch_no > 0) {
       a.snap_token = e->S.snap_token;
       a.snap_target = e->batch_no;
+      a.snap_parts = kCluster;
     }
     if (e->batch_no > 1 && e->spec_find) {  // two snapshots exist: screen speculatively
       const int cur = e->S.snap, prev = cur ^ 1;

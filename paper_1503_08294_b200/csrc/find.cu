@@ -534,17 +534,25 @@ __global__ void __launch_bounds__(32 * kW, 2) find_small_f32_kernel(FindArgs a, 
   bool waited = false;
   bool verdict = false;  // the update's: the speculative candidates stand
   if (a.snap_token) {
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: lane q polls the flag of update CTA q
+      const int lane = threadIdx.x;
+      const bool mine = lane < a.snap_parts;
       int spins = 0;
-      int t;
+      int t = 0;
+      bool done;
       do {
-        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token) : "memory");
-        if ((t >> 1) - a.snap_target >= 0) break;
-        __nanosleep(64);
+        if (mine)
+          asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token + lane) : "memory");
+        done = __all_sync(0xffffffffu, !mine || (t >> 1) - a.snap_target >= 0);
+        if (done) break;
+        __nanosleep(32);
       } while (++spins < (1 << 20));
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire after the token
-      s_ok = (t >> 1) - a.snap_target >= 0;
-      s_verdict = s_ok && (t >> 1) == a.snap_target && (t & 1);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire after the flags
+      const bool v = __all_sync(0xffffffffu, !mine || ((t >> 1) == a.snap_target && (t & 1)));
+      if (lane == 0) {
+        s_ok = done;
+        s_verdict = done && v;
+      }
     }
     __syncthreads();
     waited = !s_ok;

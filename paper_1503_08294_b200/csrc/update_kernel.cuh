@@ -985,18 +985,10 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 // publishes without reading anything else.
 __device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no, bool part_ok) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long inc = 1ull + ((unsigned long long)(part_ok ? 0u : 1u) << 32);
-    const unsigned long long old = atomicAdd(&S.cnt->snap_word, inc);
-    if (((unsigned)old + 1u) % kCluster == 0) {
-      const unsigned fails = (unsigned)(old >> 32) + (part_ok ? 0u : 1u);
-      __threadfence();
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token),
-                   "r"(2 * batch_no + (fails == 0u ? 1 : 0))
-                   : "memory");
-    }
-  }
+  if (threadIdx.x == 0)  // (release: covers the CTA's snapshot stores, ordered by the barrier)
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token + crank_of()),
+                 "r"(2 * batch_no + (part_ok ? 1 : 0))
+                 : "memory");
 }
 
 // the next batch's silent-sweep value: minimum last_active over live units
@@ -1110,7 +1102,6 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     c->nwalk = 0;
     c->fpm_bits[S.snap] = 0u;
     c->snap_disp[S.snap] = 0u;
-    c->snap_word = 0ull;  // (a multiple of the cluster size: the arrival count restarts)
   }
   // every CTA of the cluster must have started before the first DSMEM
   // exchange; the lead's resets above are read only after later barriers
