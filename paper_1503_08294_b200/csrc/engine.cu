@@ -736,6 +736,11 @@ __device__ unsigned long long g_tlu[8192][3];
 extern "C" int gs_debug_tl_update(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, g_tlu, sizeof(unsigned long long) * 3 * (size_t)n);
 }
+// per batch, the latest CTA's: last cluster barrier passed, snapshot flag posted
+__device__ unsigned long long g_tlu2[8192][2];
+extern "C" int gs_debug_tl_update2(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_tlu2, sizeof(unsigned long long) * 2 * (size_t)n);
+}
 #endif
 #include "update_kernel.cuh"
 

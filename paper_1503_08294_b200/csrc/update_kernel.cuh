@@ -879,6 +879,9 @@ __device__ __forceinline__ void csync() {
 __device__ __forceinline__ void carrive_relaxed() {
   if constexpr (kCluster > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void carrive_release() {
+  if constexpr (kCluster > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cwait() {
   if constexpr (kCluster == 1) {
     __syncthreads();
@@ -985,10 +988,16 @@ __device__ long long cl_min_ll(long long v, long long* s_ll32, long long (*s_cta
 // publishes without reading anything else.
 __device__ __forceinline__ void snapshot_arrive(const DevState& S, int batch_no, bool part_ok) {
   __syncthreads();
-  if (threadIdx.x == 0)  // (release: covers the CTA's snapshot stores, ordered by the barrier)
+  if (threadIdx.x == 0) {  // (release: covers the CTA's snapshot stores, ordered by the barrier)
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(S.snap_token + crank_of()),
                  "r"(2 * batch_no + (part_ok ? 1 : 0))
                  : "memory");
+#ifdef GS_PROF_TL
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&g_tlu2[batch_no & 8191][1], t);
+#endif
+  }
 }
 
 // the next batch's silent-sweep value: minimum last_active over live units
@@ -1621,12 +1630,50 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     atomicAdd((unsigned long long*)&c->cyc_serial, (unsigned long long)acc[12]);
     atomicAdd((unsigned long long*)&c->cyc_total, (unsigned long long)(clock64() - t_kernel));
   }
-  csync();  // the last window's walk stores are visible to the snapshot below
+  // The snapshot's row structure is stable by now: rows, their count, unit
+  // liveness and next_id change only on the event path, which every window
+  // ended with a cluster barrier after; the other slot's snapshot is the
+  // previous launch's.  Their loads go between the barrier's arrive and its
+  // wait (they overlap it), so only the positions (the walks' stores) and
+  // last_active (C1's) are loaded after it.
+  carrive_release();
+  const int sn_n = c->nrows;
+  const int sn_nid = c->next_id;
+  const int sn_gen = c->row_gen;
+  const int sn_dead = c->ndead_rows;
+  const bool same_rows = c->snap_gen[S.snap ^ 1] == sn_gen && c->rowpos_n[S.snap ^ 1] == sn_n;
+  const unsigned sn_disp = c->snap_disp[S.snap ^ 1];
+  const int sn_u00 = sn_n > 0 ? S.rows[0] : -1;
+  const bool sn_al0 = sn_u00 >= 0 && S.alive[sn_u00];
+  int sn_u[2] = {-1, -1};  // this thread's first pair of rows: units (-1: dead / none) ...
+  double sn_pv[2][3];      // ... and their previous snapshot positions
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = 2 * g + h;
+    sn_pv[h][0] = sn_pv[h][1] = sn_pv[h][2] = 0.0;
+    if (r < sn_n) {
+      const int u = S.rows[r];
+      sn_u[h] = S.alive[u] ? u : -1;
+      if (same_rows) {
+        sn_pv[h][0] = S.rowpos_prev[r];
+        sn_pv[h][1] = S.rowpos_prev[(size_t)S.U + r];
+        sn_pv[h][2] = S.rowpos_prev[2 * (size_t)S.U + r];
+      }
+    }
+  }
+  cwait();  // the last window's walk stores are visible to the snapshot below
+#ifdef GS_PROF_TL
+  if (tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&g_tlu2[batch_no & 8191][0], t);
+  }
+#endif
   // unit g's last_active / liveness for the next batch's silent-sweep value,
   // loaded with the snapshot's loads (reduced after it)
   long long la_g = -1;
   bool al_g = false;
-  if (g < c->next_id) {
+  if (g < sn_nid) {
     la_g = S.la_val[g];
     al_g = S.alive[g] != 0;
   }
@@ -1672,32 +1719,28 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     // screened find's FP32 unit pairs {-2P'x, -2P'y, -2P'z, |P'|^2} relative
     // to row 0 rounded to FP32 (dead or non-finite rows: +inf, left out of
     // the max-norm bound); every CTA takes a slice of the pairs
-    const int n = c->nrows;
+    const int n = sn_n;
     const size_t U = (size_t)S.U;
     double cx = 0.0, cy = 0.0, cz = 0.0;
-    if (n > 0) {
-      const int u0 = S.rows[0];
-      if (S.alive[u0]) {
-        const double4 p0 = S.pos[u0];
-        if (fabs(p0.x) < 1e30 && fabs(p0.y) < 1e30 && fabs(p0.z) < 1e30) {
-          cx = (double)__double2float_rn(p0.x);
-          cy = (double)__double2float_rn(p0.y);
-          cz = (double)__double2float_rn(p0.z);
-        }
+    if (sn_al0) {
+      const double4 p0 = S.pos[sn_u00];
+      if (fabs(p0.x) < 1e30 && fabs(p0.y) < 1e30 && fabs(p0.z) < 1e30) {
+        cx = (double)__double2float_rn(p0.x);
+        cy = (double)__double2float_rn(p0.y);
+        cz = (double)__double2float_rn(p0.z);
       }
     }
     if (lead) {
       c->fcen[S.snap][0] = cx;
       c->fcen[S.snap][1] = cy;
       c->fcen[S.snap][2] = cz;
-      c->snap_gen[S.snap] = c->row_gen;
+      c->snap_gen[S.snap] = sn_gen;
     }
     // the rows' displacement since the other slot's snapshot (same rows only;
     // the next find's speculative screen checks it against its bound)
-    const bool same_rows = c->snap_gen[S.snap ^ 1] == c->row_gen && c->rowpos_n[S.snap ^ 1] == n;
     double dmax = same_rows ? 0.0 : INFINITY;
     // the next find's bound (its rule: 2 x the previous update's displacement)
-    const float dspec_part = __fadd_ru(__fmul_ru(2.f, __uint_as_float(c->snap_disp[S.snap ^ 1])), 1e-30f);
+    const float dspec_part = __fadd_ru(__fmul_ru(2.f, __uint_as_float(sn_disp)), 1e-30f);
     const int np64 = (((n + 1) / 2) + 63) & ~63;
     float4* A0 = S.rowf;
     float4* A1 = S.rowf + S.rowf_stride;
@@ -1710,15 +1753,18 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
         ax[h] = ay[h] = az[h] = 0.f;
         w[h] = INFINITY;
         if (r < n) {
-          const int u = S.rows[r];
+          const bool first = p == g;  // (rows and liveness loaded before the barrier)
+          const int u = first ? sn_u[h] : (S.alive[S.rows[r]] ? S.rows[r] : -1);
           double4 q = make_double4(INFINITY, INFINITY, INFINITY, 0.0);
-          if (S.alive[u]) q = S.pos[u];
+          if (u >= 0) q = S.pos[u];
           S.rowpos[r] = q.x;
           S.rowpos[U + r] = q.y;
           S.rowpos[2 * U + r] = q.z;
           if (same_rows) {
-            const double dx = q.x - S.rowpos_prev[r], dy = q.y - S.rowpos_prev[U + r],
-                         dz = q.z - S.rowpos_prev[2 * U + r];
+            const double px0 = first ? sn_pv[h][0] : S.rowpos_prev[r];
+            const double py0 = first ? sn_pv[h][1] : S.rowpos_prev[U + r];
+            const double pz0 = first ? sn_pv[h][2] : S.rowpos_prev[2 * U + r];
+            const double dx = q.x - px0, dy = q.y - py0, dz = q.z - pz0;
             const double d2 = dx * dx + dy * dy + dz * dz;
             if (d2 == d2) dmax = fmax(dmax, d2);  // (dead rows: inf - inf)
           }
@@ -1762,9 +1808,9 @@ __global__ void GS_CLUSTER_DIMS __launch_bounds__(kUpdThreads, 1)
     next_minla(S, batch_no, mla_w);
     return;
   }
-  if (tid == 0) c->rowpos_n[S.snap] = c->nrows;
+  if (tid == 0) c->rowpos_n[S.snap] = sn_n;
   // compact rows when dead entries exceed 1/8 (keeps id order); CTA 0 only
-  if (c->ndead_rows * 8 > c->nrows) {
+  if (sn_dead * 8 > sn_n) {
     if (tid == 0) c->rowpos_n[S.snap] = -1;  // the rows move: the next find gathers
     const int n = c->nrows;
     int out = 0;
