@@ -294,6 +294,12 @@ __device__ __forceinline__ void sf_store_signals(const FindArgs& a, int64_t sig0
   }
 }
 
+#ifndef GS_POLL_NS
+#define GS_POLL_NS 32  // back-off between polls of the update's flags
+#endif
+#ifndef GS_POLL_ACQ
+#define GS_POLL_ACQ 0  // acquire loads in the poll instead of a fence after it
+#endif
 #ifdef GS_PROF_TL
 // timeline profiling builds: globaltimer stamps of every CTA for launches
 // [GS_PROF_TL - 100, GS_PROF_TL + 3), printed (tools/timeline.py parses them)
@@ -306,6 +312,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define SF_TL(k) if (threadIdx.x == 0) tl[k] = gtimer()
 // per batch: wait released (CTA 0), last CTA's end, CTA count
 __device__ unsigned long long g_tlf[8192][3];
+// per batch, CTA 0's entry and poll start; the latest CTA's poll start
+__device__ unsigned long long g_tlf2[8192][3];
+extern "C" int gs_debug_tl_find2(unsigned long long* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, g_tlf2, sizeof(unsigned long long) * 3 * (size_t)n);
+}
 extern "C" int gs_debug_tl_find(unsigned long long* out, int n) {
   return (int)cudaMemcpyFromSymbol(out, g_tlf, sizeof(unsigned long long) * 3 * (size_t)n);
 }
@@ -531,6 +542,17 @@ __global__ void __launch_bounds__(32 * kW, 2) find_small_f32_kernel(FindArgs a, 
   // launched as a programmatic dependent of the previous kernel (the update):
   // every CTA may already be resident; start once the update's row snapshot
   // is published (its token), or when that grid has completed
+#ifdef GS_PROF_TL
+  if (threadIdx.x == 0 && a.tl_batch >= 0) {
+    const unsigned long long tp = gtimer();
+    unsigned long long* g2 = g_tlf2[a.tl_batch & 8191];
+    if (blockIdx.x == 0) {
+      g2[0] = tl[0];
+      g2[1] = tp;
+    }
+    atomicMax(&g2[2], tp);
+  }
+#endif
   bool waited = false;
   bool verdict = false;  // the update's: the speculative candidates stand
   if (a.snap_token) {
@@ -541,13 +563,22 @@ __global__ void __launch_bounds__(32 * kW, 2) find_small_f32_kernel(FindArgs a, 
       int t = 0;
       bool done;
       do {
-        if (mine)
+        if (mine) {
+#if GS_POLL_ACQ
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token + lane) : "memory");
+#else
           asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(t) : "l"(a.snap_token + lane) : "memory");
+#endif
+        }
         done = __all_sync(0xffffffffu, !mine || (t >> 1) - a.snap_target >= 0);
         if (done) break;
-        __nanosleep(32);
+#if GS_POLL_NS > 0
+        __nanosleep(GS_POLL_NS);
+#endif
       } while (++spins < (1 << 20));
+#if !GS_POLL_ACQ
       asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire after the flags
+#endif
       const bool v = __all_sync(0xffffffffu, !mine || ((t >> 1) == a.snap_target && (t & 1)));
       if (lane == 0) {
         s_ok = done;

@@ -25,6 +25,11 @@ u2 = np.zeros((8192, 2), np.uint64)
 lib.gs_debug_tl_find(f.ctypes.data_as(C.c_void_p), 8192)
 lib.gs_debug_tl_update(u.ctypes.data_as(C.c_void_p), 8192)
 lib.gs_debug_tl_update2(u2.ctypes.data_as(C.c_void_p), 8192)
+f2 = np.zeros((8192, 3), np.uint64)
+has_f2 = hasattr(lib, "gs_debug_tl_find2")
+if has_f2:
+    lib.gs_debug_tl_find2(f2.ctypes.data_as(C.c_void_p), 8192)
+f2 = f2.astype(np.float64)
 f, u, u2 = f.astype(np.float64), u.astype(np.float64), u2.astype(np.float64)
 rows = []
 for b in range(2, n - 1):
@@ -32,9 +37,10 @@ for b in range(2, n - 1):
         continue
     t0 = u[b, 1]
     rows.append((b, (u2[b, 0] - t0) / 1e3, (u2[b, 1] - t0) / 1e3, (u[b, 2] - t0) / 1e3,
-                 (f[b + 1, 0] - t0) / 1e3))
+                 (f[b + 1, 0] - t0) / 1e3, (f2[b + 1, 0] - t0) / 1e3, (f2[b + 1, 1] - t0) / 1e3,
+                 (f2[b + 1, 2] - t0) / 1e3))
 r = np.array(rows)
-print("batches  last_barrier  last_flag  cta0_end  next_find_release  (us after the update's start)")
+print("batches  last_barrier  last_flag  cta0_end  next_find_release  find0_entry  find0_poll  findlast_poll  (us after the update's start)")
 for lo, hi in [(0, 130), (130, 650), (650, 2000), (2000, 8192)]:
     m = (r[:, 0] >= lo) & (r[:, 0] < hi)
     if m.any():
