@@ -113,7 +113,8 @@ struct Counters {
   // written): the silent-sweep test's value for a first window the find
   // resolved
   long long minla_next[2];
-  // (row snapshot hand-off: S.snap_token, one flag per update CTA)
+  // (unused since the row snapshot hand-off moved to per-CTA flags in
+  // S.snap_token; kept so the counters keep their cache-line layout)
   unsigned long long snap_word_unused;
   int halt_on_converge, halted;  // asynchronous runs: later batches become no-ops
   long long batches;             // update kernels that ran (not halted)
